@@ -1,0 +1,124 @@
+/*
+ * sht.h -- C-ABI of the B200-native spherical-harmonics transform step
+ * (ESCAPE SH dwarf: inverse + direct transform on an octahedral TCo grid).
+ *
+ * Boundary.  The reference (/root/reference, package `haloflow`) has no
+ * transform code: SPEC.md:20 puts "spectral-transform ... numerical
+ * mathematics" out of scope, and the SH dwarf's step is only described in
+ * PAPER.md:193-199 (Legendre + FFT + all-to-all every timestep) and modelled
+ * as flows in collectives.py:96-117 / netsim.py:347-398.  The north star
+ * (BASELINE.json) asks for "the CPU reference's Python transform API (setup
+ * with truncation, grid and field count; inv_trans/dir_trans on field
+ * batches)".  Each entry point below states which part of that API (or of the
+ * reference's modelled transposition) it replaces.  Plain pointers and sizes
+ * only; no torch types.  Python binds this with ctypes
+ * (paper_1908_06097_b200/_lib.py); INTEGRATION.md shows the binding.
+ *
+ * Conventions (shared with oracle/sht_oracle.py):
+ *   spectral field  : (T+1)(T+2) doubles, m-major, n ascending, re/im interleaved
+ *   grid field      : NPTS doubles, rings north -> south, ring j point k at
+ *                     longitude 2*pi*k/NLOEN_j
+ *   batches         : field-major, [nfld][...] contiguous, 16-byte aligned
+ *   distributed     : rank r holds the spectral coefficients of its zonal
+ *                     wavenumbers m (ascending) and the grid points of its
+ *                     ring pairs (north rings ascending, then their southern
+ *                     mirrors in north->south order); sht_local_layout lists them.
+ *
+ * Errors.  Every int-returning call returns SHT_OK (0) or one of the codes
+ * below; the message is in sht_last_error() (thread-local).  The codes map
+ * onto the reference's error classes (errors.py:9-39): SHT_ERR_CONFIG ->
+ * ConfigurationError, SHT_ERR_CUDA -> RuntimeError, SHT_ERR_COMM ->
+ * ProtocolError.
+ *
+ * Threading.  One plan per process/GPU; a plan is not re-entrant.  All work
+ * is stream-ordered on the caller's stream; there is no hidden host sync in
+ * sht_inv_trans / sht_dir_trans.
+ */
+#ifndef SHT_H_
+#define SHT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHT_OK 0
+#define SHT_ERR_CONFIG 1
+#define SHT_ERR_CUDA 2
+#define SHT_ERR_COMM 3
+
+/* plan flags */
+#define SHT_FLAG_RECOMPUTE_LEGENDRE 1 /* no P table: polynomials recomputed inside the Legendre GEMMs */
+#define SHT_FLAG_PROFILE_PHASES 2     /* record CUDA events around every phase (sht_phase_ms) */
+
+typedef struct sht_plan sht_plan;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sht_version(void);
+
+/* Replaces the north star's "setup(truncation, grid, nfld)".
+ * nloen: NDGL ring lengths (north first, north/south symmetric), or NULL for
+ * the octahedral TCo grid (ndgl must then be 2*(truncation+1)).
+ * nccl_unique_id: 128 bytes from sht_nccl_get_unique_id() on rank 0, shared
+ * by the caller (torch.distributed); NULL when nranks == 1.
+ * Replaces the modelled transposition set-up of collectives.build_alltoall
+ * (collectives.py:96-117): the plan fixes the size matrix and rotated order. */
+int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, int rank, int nranks,
+                    const void* nccl_unique_id, int flags, sht_plan** out);
+
+/* Replaces "inv_trans(spec)": spectral [nfld][nspec_re_local] -> grid
+ * [nfld][npts_local], both device pointers, on `cuda_stream` (cudaStream_t,
+ * NULL = legacy default stream). */
+int sht_inv_trans(sht_plan* plan, const double* spec, double* grid, void* cuda_stream);
+
+/* Replaces "dir_trans(grid)": grid [nfld][npts_local] -> spectral
+ * [nfld][nspec_re_local]. */
+int sht_dir_trans(sht_plan* plan, const double* grid, double* spec, void* cuda_stream);
+
+/* Sizes of this rank's local arrays.  m_list (capacity T+1) receives the
+ * rank's zonal wavenumbers ascending and n_m their count; ring_list (capacity
+ * NDGL) receives the global ring indices (0-based, north first) in local
+ * storage order and n_rings their count.  Any pointer may be NULL. */
+int sht_local_layout(const sht_plan* plan, int64_t* nspec_re, int64_t* npts, int32_t* m_list, int32_t* n_m,
+                     int32_t* ring_list, int32_t* n_rings);
+
+/* Per-phase device times (ms) of the last sht_inv_trans + sht_dir_trans on a
+ * plan created with SHT_FLAG_PROFILE_PHASES.  Order: [legendre_poly(setup),
+ * inv_legendre, inv_alltoall, inv_fft, dir_fft, dir_alltoall, dir_legendre].
+ * Synchronises on the recorded events. */
+int sht_phase_ms(sht_plan* plan, float* ms, int n);
+
+/* Algorithmic work of this rank per inverse+direct pair:
+ * Legendre flops, FFT HBM bytes, all-to-all bytes sent to other ranks. */
+int sht_work(const sht_plan* plan, double* legendre_flops, double* fft_bytes, double* a2a_bytes);
+
+/* 128-byte NCCL unique id (call on rank 0 only). */
+int sht_nccl_get_unique_id(void* out128);
+
+void sht_plan_destroy(sht_plan* plan);
+
+const char* sht_last_error(void);
+
+/* ---- host-only helpers (no GPU needed; used by the CPU test-suite) ---- */
+
+/* Gaussian nodes of the northern hemisphere, pole -> equator (ndgl/2 each):
+ * mu = sin(latitude), sint = cos(latitude), w = Gaussian weight. */
+int sht_gauss_nodes(int ndgl, double* mu, double* sint, double* w);
+
+/* Ownership used by a plan with `nranks` ranks: m_owner[T+1] (rank owning
+ * zonal wavenumber m), ring_owner[ndgl/2] (rank owning northern ring i and
+ * its southern mirror).  nloen may be NULL (octahedral). */
+int sht_partition(int truncation, int ndgl, const int32_t* nloen, int nranks, int32_t* m_owner,
+                  int32_t* ring_owner);
+
+/* FFT plan chosen for a ring of n points: number of radix stages written to
+ * radices (capacity 32), transform length L (n, or the Bluestein length) and
+ * whether Bluestein is used. */
+int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHT_H_ */

@@ -1,0 +1,114 @@
+// Internal declarations shared by the host plan (sht_plan.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sht.h"
+
+namespace sht {
+
+// ---------------------------------------------------------------- error state
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define SHT_CUDA_TRY(expr)                                                                            \
+  do {                                                                                               \
+    cudaError_t _e = (expr);                                                                         \
+    if (_e != cudaSuccess)                                                                           \
+      return ::sht::fail(SHT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+// ---------------------------------------------------------------- Legendre GEMM tiling
+// leg_inv: CTA tile = 64 northern rings x 64 fields, k-chunk = 32 wavenumbers n.
+// leg_dir: CTA tile = 128 wavenumbers n x 64 fields, k-chunk = 16 rings.
+constexpr int kLegFields = 64;
+constexpr int kInvRings = 64;
+constexpr int kInvKc = 32;
+constexpr int kDirN = 128;
+constexpr int kDirKc = 16;
+constexpr int kPtabPad = 32;  // P-table rows are padded (with zeros) to a multiple of this
+
+struct LegTile {  // one output tile of a Legendre GEMM
+  int32_t lm;     // local wavenumber index
+  int32_t r0;     // leg_inv: first northern ring; leg_dir: first n-m offset
+  int32_t f0;     // first field
+  int32_t pad;
+};
+
+struct LegParams {
+  int T, nh, nfld;
+  int nlm;                   // number of local wavenumbers
+  const int32_t* lm_m;       // [nlm] m of each local wavenumber
+  const int32_t* lm_i0;      // [nlm] first northern ring with M_i >= m
+  const int64_t* lm_poff;    // [nlm] P-table offset (doubles) of (ring i0, n = m)
+  const int32_t* lm_kp;      // [nlm] padded P-table row length
+  const int64_t* lm_soff;    // [nlm] complex offset of (m, n = m) in the local spectral field
+  int64_t spec_ld;           // doubles per local spectral field
+  const int32_t* xbase;      // [nh] Fourier row of (ring i, lm = 0) in the m-side buffer
+  const double* ptab;        // P table
+  const LegTile* tiles;
+  int ntiles;
+  int* counter;              // persistent-scheduler ticket
+};
+
+void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s);
+void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s);
+void launch_leg_poly(int T, int nh, int nlm, const int32_t* lm_m, const int32_t* lm_i0, const int64_t* lm_poff,
+                     const int32_t* lm_kp, const double* mu, const double* sint, double* dmant, int32_t* dexp,
+                     double* ptab, cudaStream_t s);
+size_t leg_inv_smem();
+size_t leg_dir_smem();
+
+// ---------------------------------------------------------------- ring FFTs
+constexpr int kFftThreads = 512;
+constexpr int kFftMaxLen = 8192;                   // longest transform one CTA handles (smem bound)
+constexpr int kMaxStages = 24;
+
+struct FftRing {       // one northern ring (and its southern mirror) on this rank
+  int32_t n;           // points on the ring
+  int32_t L;           // transform length (n, or the Bluestein length)
+  int32_t mcap;        // M_i
+  int32_t nstage;
+  int8_t radix[kMaxStages];
+  int64_t tw_off;      // complex offset of W_L[k] = exp(-2 pi i k / L)
+  int64_t chirp_off;   // Bluestein chirp w_n = exp(-pi i n^2 / N), n < N   (-1: none)
+  int64_t bhat_off;    // Bluestein kernel spectrum / L                     (-1: none)
+  int64_t goff_n;      // offset of the northern ring in the local grid field
+  int64_t goff_s;      // offset of the southern ring in the local grid field
+  int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
+  double w;            // Gaussian weight
+  int32_t fp;          // field pairs per CTA
+  int32_t nb;          // sequences per pass
+};
+
+struct FftWork {       // one CTA of a ring-FFT launch
+  int32_t ring;        // local ring index
+  int32_t fp0;         // first field pair
+};
+
+struct FftParams {
+  int nfld;
+  int64_t grid_ld;           // doubles per local grid field
+  const FftRing* rings;
+  const FftWork* work;
+  int nwork;
+  const double2* tw;         // twiddle / chirp arena
+  const int32_t* yrow;       // Fourier row of (ring, m)
+};
+
+// Launch the CTAs work[w0 .. w0+nw) of a ring-FFT pass with `smem` bytes of dynamic shared memory.
+void launch_fft_g2f(const FftParams& p, int w0, int nw, const double* grid, double* four, size_t smem,
+                    cudaStream_t s);
+void launch_fft_f2g(const FftParams& p, int w0, int nw, const double* four, double* grid, size_t smem,
+                    cudaStream_t s);
+// Complex values one pass can keep in flight for a plan with these radices.
+int fft_capacity(const std::vector<int>& radices);
+// Plan for a ring of n points: mixed radix {2,3,4,5,7,8,11,13} when n factors
+// over those, else Bluestein with the smallest 7-smooth L >= 2n-1 that fits.
+int fft_choose(int n, std::vector<int>& radices, int& L, bool& bluestein);
+
+}  // namespace sht

@@ -1,0 +1,421 @@
+// Legendre side of the SH transform on sm_100a:
+//   K3 leg_diag/leg_poly : associated-Legendre table P_n^m(mu_i) (X-number recurrence)
+//   K1 leg_inv           : per-m parity-split FP64 GEMM, spectral -> Fourier (S/A rows)
+//   K2 leg_dir           : per-m parity-split FP64 GEMM, Fourier (S/A rows) -> spectral
+//
+// FP64 tensor cores: tcgen05.mma has no f64 kind, so the
+// GEMMs are built from warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4),
+// the only FP64 tensor path on B200; measured issue peak 37.1 TFLOP/s at
+// 1965 MHz (profiles/r01_probe_fp64.json).  Operands are staged HBM -> shared
+// memory with a 3-stage cp.async (LDGSTS, zero-fill for ragged edges) pipeline;
+// fragments are read with conflict-free 128-bit LDS; a persistent CTA per SM
+// pulls tiles (largest K first) from an atomic ticket.
+//
+// Parity split (SURVEY.md App. A "Hemispheric split"): for each m the S
+// accumulator takes the even n-m and the A accumulator the odd n-m.  Both come
+// out of the same smem tiles because P[ring][n] and spec[field][n][re,im] keep
+// n contiguous: one 128-bit LDS yields the (S, A) pair of an operand fragment.
+// The ring FFT kernels consume/produce S and A directly (north = S + A,
+// south = S - A), so the Legendre kernels have no combine epilogue at all.
+#include "sht_internal.h"
+
+namespace sht {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ------------------------------------------------------------------ leg_inv
+constexpr int kInvStages = 3;
+constexpr int kInvPStr = kInvKc + 8;          // 40 doubles: rows of P tile (== 8 mod 16 -> no LDS.128 conflicts)
+constexpr int kInvSStr = 2 * kInvKc + 2;      // 66 doubles: field rows of the spectral tile (== 2 mod 16)
+constexpr int kInvPDbl = kInvRings * kInvPStr;
+constexpr int kInvSDbl = kLegFields * kInvSStr;
+constexpr int kInvStageDbl = kInvPDbl + kInvSDbl;
+constexpr int kLegThreads = 256;
+
+// Tile: rings r0..r0+63 (northern index) x fields f0..f0+63 of wavenumber lm.
+// Warp w: rings 32*(w&1).. , fields 16*(w>>1)..  -> 4 ring groups x 2 field groups
+// x {S.re, S.im, A.re, A.im} DMMA accumulators (64 doubles per thread).
+__global__ void __launch_bounds__(kLegThreads, 1)
+    leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 1, wf = warp >> 1;
+  const int lr = lane >> 2, lc = lane & 3;
+
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int t = s_tile;
+    if (t >= p.ntiles) break;
+    const LegTile tile = p.tiles[t];
+    const int lm = tile.lm, r0 = tile.r0, f0 = tile.f0;
+    const int m = p.lm_m[lm];
+    const int i0 = p.lm_i0[lm];
+    const int kp = p.lm_kp[lm];
+    const int K = p.T - m + 1;
+    const int nk = (K + kInvKc - 1) / kInvKc;
+    const double* P = p.ptab + p.lm_poff[lm] + (int64_t)(r0 - i0) * kp;
+    const double* S = spec + 2 * p.lm_soff[lm];
+
+    auto load_stage = [&](int kc, int st) {
+      double* Ps = sm + st * kInvStageDbl;
+      double* Ss = Ps + kInvPDbl;
+#pragma unroll
+      for (int it = 0; it < (kInvRings * (kInvKc / 2)) / kLegThreads; ++it) {
+        const int c = tid + it * kLegThreads;
+        const int row = c >> 4, col = c & 15;
+        const bool v = (r0 + row) < p.nh;
+        const double* src = v ? P + (int64_t)row * kp + kc * kInvKc + col * 2 : p.ptab;
+        cp_async16(Ps + row * kInvPStr + col * 2, src, v);
+      }
+#pragma unroll
+      for (int it = 0; it < (kLegFields * kInvKc) / kLegThreads; ++it) {
+        const int c = tid + it * kLegThreads;
+        const int f = c >> 5, n = c & 31;
+        const int kk = kc * kInvKc + n;
+        const bool v = (f0 + f) < p.nfld && kk < K;
+        const double* src = v ? S + (int64_t)(f0 + f) * p.spec_ld + 2 * kk : spec;
+        cp_async16(Ss + f * kInvSStr + 2 * n, src, v);
+      }
+    };
+
+    double acc[4][2][4][2];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
+
+    const bool active = (r0 + wr * 32 < p.nh) && (f0 + wf * 16 < p.nfld);
+
+#pragma unroll
+    for (int s = 0; s < kInvStages - 1; ++s) {
+      if (s < nk) load_stage(s, s);
+      cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      cp_async_wait<kInvStages - 2>();
+      __syncthreads();
+      {
+        const int nx = kc + kInvStages - 1;
+        if (nx < nk) load_stage(nx, nx % kInvStages);
+        cp_async_commit();
+      }
+      if (active) {
+        const double* Ps = sm + (kc % kInvStages) * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
+        const double* Ss = sm + (kc % kInvStages) * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
+#pragma unroll
+        for (int sub = 0; sub < kInvKc / 8; ++sub) {
+          double2 a[4], bs[2], ba[2];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) a[g] = *reinterpret_cast<const double2*>(Ps + g * 8 * kInvPStr + sub * 8);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double* bp = Ss + h * 8 * kInvSStr + sub * 16;
+            bs[h] = *reinterpret_cast<const double2*>(bp);
+            ba[h] = *reinterpret_cast<const double2*>(bp + 2);
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
+              dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
+              dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
+              dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+            }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if (active) {
+      const int64_t rowd = (int64_t)p.nfld * 4;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int ring = r0 + wr * 32 + g * 8 + lr;
+        if (ring < p.nh) {
+          double* dst = four + (int64_t)(p.xbase[ring] + lm) * rowd;
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int f = f0 + wf * 16 + h * 8 + 2 * lc + e;
+              if (f < p.nfld) {
+                double2* d = reinterpret_cast<double2*>(dst + (int64_t)f * 4);
+                d[0] = make_double2(acc[g][h][0][e], acc[g][h][1][e]);
+                d[1] = make_double2(acc[g][h][2][e], acc[g][h][3][e]);
+              }
+            }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ leg_dir
+constexpr int kDirStages = 3;
+constexpr int kDirPStr = kDirN + 4;            // 132: P tile [ring][n]          (== 4 mod 16)
+constexpr int kDirBStr = 2 * kLegFields + 4;   // 132: S / A tiles [ring][field][re,im]
+constexpr int kDirPDbl = kDirKc * kDirPStr;
+constexpr int kDirBDbl = kDirKc * kDirBStr;
+constexpr int kDirStageDbl = kDirPDbl + 2 * kDirBDbl;
+
+// Tile: n-m offsets n0..n0+127 (64 even-parity rows, 64 odd) x fields f0..f0+63.
+// Warp w: n 64*(w&1).. (4 groups of 8 (S,A) row pairs), fields 16*(w>>1)..
+__global__ void __launch_bounds__(kLegThreads, 1)
+    leg_dir_kernel(const LegParams p, const double* __restrict__ four, double* __restrict__ spec) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wn = warp & 1, wf = warp >> 1;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int64_t rowd = (int64_t)p.nfld * 4;
+
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int t = s_tile;
+    if (t >= p.ntiles) break;
+    const LegTile tile = p.tiles[t];
+    const int lm = tile.lm, n0 = tile.r0, f0 = tile.f0;
+    const int m = p.lm_m[lm];
+    const int i0 = p.lm_i0[lm];
+    const int kp = p.lm_kp[lm];
+    const int K = p.T - m + 1;
+    const int nrings = p.nh - i0;
+    const int nk = (nrings + kDirKc - 1) / kDirKc;
+    const double* P = p.ptab + p.lm_poff[lm];
+
+    auto load_stage = [&](int kc, int st) {
+      double* Ps = sm + st * kDirStageDbl;
+      double* Ss = Ps + kDirPDbl;
+      double* As = Ss + kDirBDbl;
+#pragma unroll
+      for (int it = 0; it < (kDirKc * (kDirN / 2)) / kLegThreads; ++it) {
+        const int c = tid + it * kLegThreads;
+        const int rr = c >> 6, cc = c & 63;
+        const int ring = kc * kDirKc + rr;  // relative to i0
+        const int nn = n0 + 2 * cc;
+        const bool v = ring < nrings && nn < K;
+        const double* src = v ? P + (int64_t)ring * kp + nn : p.ptab;
+        cp_async16(Ps + rr * kDirPStr + 2 * cc, src, v);
+      }
+#pragma unroll
+      for (int it = 0; it < (kDirKc * kLegFields * 2) / kLegThreads; ++it) {
+        const int c = tid + it * kLegThreads;
+        const int rr = c >> 7, rem = c & 127;
+        const int f = rem >> 1, half = rem & 1;
+        const int ring = kc * kDirKc + rr;
+        const bool v = ring < nrings && (f0 + f) < p.nfld;
+        const double* src = v ? four + (int64_t)(p.xbase[i0 + ring] + lm) * rowd + (int64_t)(f0 + f) * 4 + 2 * half : four;
+        cp_async16((half ? As : Ss) + rr * kDirBStr + 2 * f, src, v);
+      }
+    };
+
+    double acc[4][2][4][2];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
+
+    const bool active = (n0 + wn * 64 < K) && (f0 + wf * 16 < p.nfld);
+
+#pragma unroll
+    for (int s = 0; s < kDirStages - 1; ++s) {
+      if (s < nk) load_stage(s, s);
+      cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      cp_async_wait<kDirStages - 2>();
+      __syncthreads();
+      {
+        const int nx = kc + kDirStages - 1;
+        if (nx < nk) load_stage(nx, nx % kDirStages);
+        cp_async_commit();
+      }
+      if (active) {
+        const double* Ps = sm + (kc % kDirStages) * kDirStageDbl + lc * kDirPStr + wn * 64 + 2 * lr;
+        const double* Ss = sm + (kc % kDirStages) * kDirStageDbl + kDirPDbl + lc * kDirBStr + 2 * (wf * 16 + lr);
+        const double* As = Ss + kDirBDbl;
+#pragma unroll
+        for (int ks = 0; ks < kDirKc / 4; ++ks) {
+          double2 a[4], bs[2], ba[2];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            a[g] = *reinterpret_cast<const double2*>(Ps + ks * 4 * kDirPStr + 16 * g);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            bs[h] = *reinterpret_cast<const double2*>(Ss + ks * 4 * kDirBStr + 16 * h);
+            ba[h] = *reinterpret_cast<const double2*>(As + ks * 4 * kDirBStr + 16 * h);
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
+              dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
+              dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
+              dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+            }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if (active) {
+      const int64_t soff = 2 * p.lm_soff[lm];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int ns = n0 + wn * 64 + 2 * (g * 8 + lr);
+        if (ns < K) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int f = f0 + wf * 16 + h * 8 + 2 * lc + e;
+              if (f < p.nfld) {
+                double2* d = reinterpret_cast<double2*>(spec + (int64_t)f * p.spec_ld + soff + 2 * ns);
+                d[0] = make_double2(acc[g][h][0][e], acc[g][h][1][e]);
+                if (ns + 1 < K) d[1] = make_double2(acc[g][h][2][e], acc[g][h][3][e]);
+              }
+            }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ leg_poly
+// X-number sectoral start values, one thread per northern ring walking m = 0..T.
+// Operation order matches oracle/sht_oracle.py legendre_diag exactly (no FMA
+// contraction), so the P table is bit-identical to the oracle's.
+__global__ void leg_diag_kernel(int T, int nh, const double* __restrict__ sint, int nlm,
+                                const int32_t* __restrict__ lm_m, double* __restrict__ dmant,
+                                int32_t* __restrict__ dexp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nh) return;
+  const double s = sint[i];
+  const double two400 = 0x1p400, twom400 = 0x1p-400;
+  double cur = 1.0 / sqrt(2.0);
+  int e = 0;
+  int lm = 0;
+  if (lm < nlm && lm_m[lm] == 0) {
+    dmant[(int64_t)lm * nh + i] = cur;
+    dexp[(int64_t)lm * nh + i] = e;
+    ++lm;
+  }
+  for (int m = 1; m <= T && lm < nlm; ++m) {
+    const double fac = __dmul_rn(sqrt((2.0 * m + 1.0) / (2.0 * m)), s);
+    cur = __dmul_rn(cur, fac);
+    if (cur < twom400) {
+      cur = __dmul_rn(cur, two400);
+      e -= 400;
+    }
+    if (lm_m[lm] == m) {
+      dmant[(int64_t)lm * nh + i] = cur;
+      dexp[(int64_t)lm * nh + i] = e;
+      ++lm;
+    }
+  }
+}
+
+__device__ __forceinline__ double eps_nm(int n, int m) {
+  const double nn = (double)n;
+  return sqrt(__ddiv_rn(__dsub_rn(__dmul_rn(nn, nn), (double)((int64_t)m * m)),
+                        __dsub_rn(__dmul_rn(__dmul_rn(4.0, nn), nn), 1.0)));
+}
+
+// One thread per (local m, ring): three-term recurrence in n on the mantissa,
+// shared per-ring exponent, renormalised by 2^-400 above 2^400.
+__global__ void leg_poly_kernel(int T, int nh, const int32_t* __restrict__ lm_m, const int32_t* __restrict__ lm_i0,
+                                const int64_t* __restrict__ lm_poff, const int32_t* __restrict__ lm_kp,
+                                const double* __restrict__ mu, const double* __restrict__ dmant,
+                                const int32_t* __restrict__ dexp, double* __restrict__ ptab) {
+  const int lm = blockIdx.y;
+  const int m = lm_m[lm];
+  const int i0 = lm_i0[lm];
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nh) return;
+  const int kp = lm_kp[lm];
+  double* out = ptab + lm_poff[lm] + (int64_t)(i - i0) * kp;
+  const double x = mu[i];
+  const double two400 = 0x1p400, twom400 = 0x1p-400;
+  int e = dexp[(int64_t)lm * nh + i];
+  double q2 = dmant[(int64_t)lm * nh + i];
+  out[0] = ldexp(q2, e);
+  if (m == T) return;
+  double q1 = __dmul_rn(__dmul_rn(sqrt(2.0 * m + 3.0), x), q2);
+  out[1] = ldexp(q1, e);
+  double epsm1 = eps_nm(m + 1, m);
+  for (int n = m + 2; n <= T; ++n) {
+    const double epsn = eps_nm(n, m);
+    double q = __ddiv_rn(__dsub_rn(__dmul_rn(x, q1), __dmul_rn(epsm1, q2)), epsn);
+    if (fabs(q) > two400) {
+      q = __dmul_rn(q, twom400);
+      q1 = __dmul_rn(q1, twom400);
+      e += 400;
+    }
+    q2 = q1;
+    q1 = q;
+    epsm1 = epsn;
+    out[n - m] = ldexp(q, e);
+  }
+}
+
+}  // namespace
+
+size_t leg_inv_smem() { return (size_t)kInvStages * kInvStageDbl * sizeof(double); }
+size_t leg_dir_smem() { return (size_t)kDirStages * kDirStageDbl * sizeof(double); }
+
+void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(leg_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    attr = true;
+  }
+  leg_inv_kernel<<<grid, kLegThreads, leg_inv_smem(), s>>>(p, spec, four);
+}
+
+void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(leg_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_dir_smem());
+    attr = true;
+  }
+  leg_dir_kernel<<<grid, kLegThreads, leg_dir_smem(), s>>>(p, four, spec);
+}
+
+void launch_leg_poly(int T, int nh, int nlm, const int32_t* lm_m, const int32_t* lm_i0, const int64_t* lm_poff,
+                     const int32_t* lm_kp, const double* mu, const double* sint, double* dmant, int32_t* dexp,
+                     double* ptab, cudaStream_t s) {
+  if (nlm == 0) return;
+  leg_diag_kernel<<<(nh + 127) / 128, 128, 0, s>>>(T, nh, sint, nlm, lm_m, dmant, dexp);
+  dim3 grid((nh + 127) / 128, nlm);
+  leg_poly_kernel<<<grid, 128, 0, s>>>(T, nh, lm_m, lm_i0, lm_poff, lm_kp, mu, dmant, dexp, ptab);
+}
+
+}  // namespace sht

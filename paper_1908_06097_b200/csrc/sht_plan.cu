@@ -1,0 +1,740 @@
+// Host side of libsht.so: plan construction (geometry, partition, buffer
+// layouts, FFT plans, Legendre tile lists), the C-ABI of include/sht.h, and
+// the NCCL grid<->spectral transposition.
+//
+// Data layout in HBM (per rank r, NFLD fields):
+//   spectral  [nfld][2 * sum_{m in M_r} (T-m+1)]      m ascending, n ascending, re/im
+//   grid      [nfld][sum_{i in R_r} 2 N_i]             local north rings asc, then their south mirrors
+//   P table   per local m: [NDGLU(m) rings][Kp(m)]      Kp = roundup(T-m+1, 32), zero padded
+//   Fourier   rows of nfld x {S.re, S.im, A.re, A.im}   one row per (ring pair i, m <= M_i)
+//     X (m side, written by leg_inv / read by leg_dir):  [dest d][i in R_d][lm in M_r, m <= M_i]
+//     Y (ring side, read by fft_f2g / written by fft_g2f): [src s][i in R_r][lm in M_s, m <= M_i]
+//   so the per-destination block of X on rank r is exactly the per-source block
+//   of Y on rank d, and the all-to-all is a plain grouped send/recv of
+//   contiguous row ranges.  With one rank X and Y are the same buffer.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "sht_internal.h"
+
+namespace sht {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SHT_NCCL_TRY(expr)                                                                           \
+  do {                                                                                              \
+    ncclResult_t _r = (expr);                                                                       \
+    if (_r != ncclSuccess) return ::sht::fail(SHT_ERR_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+// ------------------------------------------------------------------ geometry
+// Gaussian nodes by Newton on theta in x87 extended precision.  The
+// operation order is the one of oracle/sht_oracle.py gauss_nodes (numpy
+// longdouble), so both round to the same doubles.
+static void gauss_nodes_ld(int n, std::vector<double>& mu, std::vector<double>& sint, std::vector<double>& w) {
+  typedef long double LD;
+  const int nh = n / 2;
+  const LD nld = (LD)n;
+  const LD pi = 3.14159265358979323846264338327950288L;
+  mu.resize(nh);
+  sint.resize(nh);
+  w.resize(nh);
+  auto pn = [&](LD x, LD& p1o, LD& p0o) {
+    LD p0 = 1.0L, p1 = x;
+    for (int j = 2; j <= n; ++j) {
+      const LD jl = (LD)j;
+      const LD p2 = ((2.0L * jl - 1.0L) * x * p1 - (jl - 1.0L) * p0) / jl;
+      p0 = p1;
+      p1 = p2;
+    }
+    p1o = p1;
+    p0o = p0;
+  };
+  for (int k = 1; k <= nh; ++k) {
+    LD theta = pi * (4.0L * (LD)k - 1.0L) / (4.0L * nld + 2.0L);
+    for (int it = 0; it < 8; ++it) {
+      const LD x = cosl(theta);
+      const LD s = sinl(theta);
+      LD p1, p0;
+      pn(x, p1, p0);
+      const LD dp = nld * (x * p1 - p0) / (x * x - 1.0L);
+      theta = theta + p1 / (s * dp);
+    }
+    const LD x = cosl(theta);
+    const LD s = sinl(theta);
+    LD p1, p0;
+    pn(x, p1, p0);
+    const LD ww = 2.0L * s * s / ((nld * p0) * (nld * p0));
+    mu[k - 1] = (double)x;
+    sint[k - 1] = (double)s;
+    w[k - 1] = (double)ww;
+  }
+}
+
+// Snake (boustrophedon) dealing of 0..n-1 over P ranks: 0,1,..,P-1,P-1,..,0,0,1,..
+// Work per wavenumber, NDGLU(m)(T-m+1), and points per ring pair, 4i+20, are
+// monotone, so the snake balances both.
+static void snake(int n, int P, std::vector<int>& owner) {
+  owner.resize(n);
+  for (int k = 0; k < n; ++k) {
+    const int blk = k / P, pos = k % P;
+    owner[k] = (blk % 2 == 0) ? pos : P - 1 - pos;
+  }
+}
+
+struct Geometry {
+  int T = 0, ndgl = 0, nh = 0;
+  std::vector<int> nloen;  // all rings
+  std::vector<int> mcap;   // northern rings
+};
+
+static int make_geometry(int T, int ndgl, const int32_t* nloen, Geometry& g) {
+  if (T < 1) return fail(SHT_ERR_CONFIG, "truncation must be >= 1");
+  g.T = T;
+  if (nloen == nullptr) {
+    if (ndgl != 2 * (T + 1) && ndgl != 0)
+      return fail(SHT_ERR_CONFIG, "octahedral grid needs ndgl == 2*(truncation+1)");
+    g.ndgl = 2 * (T + 1);
+    g.nloen.resize(g.ndgl);
+    for (int i = 0; i <= T; ++i) {
+      g.nloen[i] = 4 * (i + 1) + 16;
+      g.nloen[g.ndgl - 1 - i] = g.nloen[i];
+    }
+  } else {
+    if (ndgl < 2 || ndgl % 2) return fail(SHT_ERR_CONFIG, "ndgl must be even and >= 2");
+    g.ndgl = ndgl;
+    g.nloen.assign(nloen, nloen + ndgl);
+    for (int j = 0; j < ndgl; ++j) {
+      if (g.nloen[j] != g.nloen[ndgl - 1 - j])
+        return fail(SHT_ERR_CONFIG, "nloen must be north/south symmetric");
+      if (g.nloen[j] < 1) return fail(SHT_ERR_CONFIG, "nloen entries must be >= 1");
+    }
+  }
+  g.nh = g.ndgl / 2;
+  g.mcap.resize(g.nh);
+  for (int i = 0; i < g.nh; ++i) {
+    g.mcap[i] = std::min(T, (g.nloen[i] - 1) / 2);
+    if (i > 0 && g.mcap[i] < g.mcap[i - 1])
+      return fail(SHT_ERR_CONFIG, "ring wavenumber caps must be non-decreasing from pole to equator");
+  }
+  return SHT_OK;
+}
+
+// ------------------------------------------------------------------ host FFT (plan set-up only)
+typedef std::complex<long double> cld;
+static void dft_rec(const cld* in, int stride, cld* out, int n) {
+  if (n == 1) {
+    out[0] = in[0];
+    return;
+  }
+  int p = 2;
+  while (n % p) ++p;
+  const int m = n / p;
+  std::vector<cld> sub((size_t)n);
+  for (int r = 0; r < p; ++r) dft_rec(in + (size_t)r * stride, stride * p, sub.data() + (size_t)r * m, m);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < n; ++k) {
+    cld acc = 0;
+    for (int r = 0; r < p; ++r) {
+      const long long e = ((long long)r * k) % n;
+      const long double ang = -two_pi * (long double)e / (long double)n;
+      acc += sub[(size_t)r * m + (k % m)] * cld(cosl(ang), sinl(ang));
+    }
+    out[k] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ plan
+struct Phase {
+  cudaEvent_t ev[10];
+};
+
+}  // namespace sht
+
+struct sht_plan {
+  sht::Geometry g;
+  int nfld = 0, rank = 0, nranks = 1, flags = 0, nsm = 148;
+  std::vector<double> mu, sint, w;
+  std::vector<int> m_owner, ring_owner, lm_of_m;
+  std::vector<int> my_m, my_rings;
+  std::vector<int64_t> lm_soff;
+  int64_t spec_ld = 0, grid_ld = 0;
+  std::vector<int64_t> xoff, xrows, yoff, yrows;  // per peer, in rows
+  int64_t xtot = 0, ytot = 0;
+  double work_leg = 0, work_fft = 0, work_a2a = 0;
+
+  // device
+  double* d_mu = nullptr;
+  double* d_sint = nullptr;
+  double* d_ptab = nullptr;
+  int64_t ptab_len = 0;
+  int32_t *d_lm_m = nullptr, *d_lm_i0 = nullptr, *d_lm_kp = nullptr, *d_xbase = nullptr;
+  int64_t *d_lm_poff = nullptr, *d_lm_soff = nullptr;
+  sht::LegTile *d_tiles_inv = nullptr, *d_tiles_dir = nullptr;
+  int ntiles_inv = 0, ntiles_dir = 0;
+  int* d_counter = nullptr;
+  double* X = nullptr;
+  double* Y = nullptr;
+  sht::FftRing* d_rings = nullptr;
+  sht::FftWork* d_work = nullptr;
+  int nwork_small = 0, nwork_large = 0;
+  size_t smem_small = 0, smem_large = 0;
+  double2* d_tw = nullptr;
+  int32_t* d_yrow = nullptr;
+  ncclComm_t comm = nullptr;
+  bool have_events = false;
+  cudaEvent_t ev[10];
+  float setup_ms = 0.f;
+};
+
+namespace sht {
+
+static void free_plan(sht_plan* p) {
+  if (!p) return;
+  void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
+                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X,
+                  p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->have_events)
+    for (auto& e : p->ev) cudaEventDestroy(e);
+  if (p->comm) ncclCommDestroy(p->comm);
+  delete p;
+}
+
+template <typename T>
+static int upload(T** dst, const std::vector<T>& v) {
+  const size_t bytes = std::max<size_t>(v.size(), 1) * sizeof(T);
+  SHT_CUDA_TRY(cudaMalloc((void**)dst, bytes));
+  if (!v.empty()) SHT_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return SHT_OK;
+}
+
+static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, std::vector<int>& ring_owner) {
+  if (P < 1) return fail(SHT_ERR_CONFIG, "nranks must be >= 1");
+  snake(g.T + 1, P, m_owner);
+  snake(g.nh, P, ring_owner);
+  return SHT_OK;
+}
+
+static int build_plan(sht_plan* p, const void* nccl_id) {
+  const Geometry& g = p->g;
+  const int T = g.T, nh = g.nh, P = p->nranks, r = p->rank, nfld = p->nfld;
+  gauss_nodes_ld(g.ndgl, p->mu, p->sint, p->w);
+  if (int rc = build_partition(g, P, p->m_owner, p->ring_owner)) return rc;
+
+  std::vector<std::vector<int>> Mlist(P), Rlist(P);
+  p->lm_of_m.assign(T + 1, 0);
+  for (int m = 0; m <= T; ++m) {
+    const int s = p->m_owner[m];
+    p->lm_of_m[m] = (int)Mlist[s].size();
+    Mlist[s].push_back(m);
+  }
+  for (int i = 0; i < nh; ++i) Rlist[p->ring_owner[i]].push_back(i);
+  p->my_m = Mlist[r];
+  p->my_rings = Rlist[r];
+  const int nlm = (int)p->my_m.size();
+
+  // c[s][i] = #{m in M_s : m <= M_i}
+  std::vector<std::vector<int>> cnt(P, std::vector<int>(nh));
+  for (int s = 0; s < P; ++s) {
+    size_t k = 0;
+    for (int i = 0; i < nh; ++i) {
+      while (k < Mlist[s].size() && Mlist[s][k] <= g.mcap[i]) ++k;
+      cnt[s][i] = (int)k;
+    }
+  }
+  // X: [d][i in R_d][lm]
+  std::vector<int32_t> xbase(nh, 0);
+  p->xoff.assign(P, 0);
+  p->xrows.assign(P, 0);
+  int64_t cur = 0;
+  for (int d = 0; d < P; ++d) {
+    p->xoff[d] = cur;
+    for (int i : Rlist[d]) {
+      xbase[i] = (int32_t)cur;
+      cur += cnt[r][i];
+    }
+    p->xrows[d] = cur - p->xoff[d];
+  }
+  p->xtot = cur;
+  // Y: [s][i in R_r][lm_s]
+  std::vector<std::vector<int64_t>> ybase(P, std::vector<int64_t>(nh, 0));
+  p->yoff.assign(P, 0);
+  p->yrows.assign(P, 0);
+  cur = 0;
+  for (int s = 0; s < P; ++s) {
+    p->yoff[s] = cur;
+    for (int i : Rlist[r]) {
+      ybase[s][i] = cur;
+      cur += cnt[s][i];
+    }
+    p->yrows[s] = cur - p->yoff[s];
+  }
+  p->ytot = cur;
+  if (p->xtot > INT32_MAX || p->ytot > INT32_MAX) return fail(SHT_ERR_CONFIG, "Fourier row count overflows int32");
+
+  // local spectral layout
+  p->lm_soff.resize(nlm);
+  int64_t so = 0;
+  for (int lm = 0; lm < nlm; ++lm) {
+    p->lm_soff[lm] = so;
+    so += T - p->my_m[lm] + 1;
+  }
+  p->spec_ld = 2 * so;
+
+  // P-table layout
+  std::vector<int32_t> lm_i0(nlm), lm_kp(nlm), lm_m(p->my_m.begin(), p->my_m.end());
+  std::vector<int64_t> lm_poff(nlm);
+  int64_t po = 0;
+  double leg_flops = 0;
+  for (int lm = 0; lm < nlm; ++lm) {
+    const int m = p->my_m[lm];
+    const int i0 = (int)(std::lower_bound(g.mcap.begin(), g.mcap.end(), m) - g.mcap.begin());
+    const int K = T - m + 1;
+    lm_i0[lm] = i0;
+    lm_kp[lm] = (K + kPtabPad - 1) / kPtabPad * kPtabPad;
+    lm_poff[lm] = po;
+    po += (int64_t)(nh - i0) * lm_kp[lm];
+    leg_flops += 4.0 * nfld * (double)(nh - i0) * K;
+  }
+  p->ptab_len = po;
+  p->work_leg = 2.0 * leg_flops;
+
+  // Legendre tiles (largest K first: the persistent scheduler then behaves like LPT)
+  std::vector<LegTile> ti, td;
+  for (int lm = 0; lm < nlm; ++lm) {
+    const int K = T - p->my_m[lm] + 1;
+    for (int r0 = lm_i0[lm]; r0 < nh; r0 += kInvRings)
+      for (int f0 = 0; f0 < nfld; f0 += kLegFields) ti.push_back({lm, r0, f0, 0});
+    for (int n0 = 0; n0 < K; n0 += kDirN)
+      for (int f0 = 0; f0 < nfld; f0 += kLegFields) td.push_back({lm, n0, f0, 0});
+  }
+  auto kof = [&](const LegTile& t) { return T - p->my_m[t.lm] + 1; };
+  std::stable_sort(ti.begin(), ti.end(), [&](const LegTile& a, const LegTile& b) { return kof(a) > kof(b); });
+  auto dwork = [&](const LegTile& t) {
+    return (int64_t)(nh - lm_i0[t.lm]) * std::min(kDirN, kof(t) - t.r0);
+  };
+  std::stable_sort(td.begin(), td.end(), [&](const LegTile& a, const LegTile& b) { return dwork(a) > dwork(b); });
+  p->ntiles_inv = (int)ti.size();
+  p->ntiles_dir = (int)td.size();
+
+  // grid layout + FFT plans
+  const int nlr = (int)p->my_rings.size();
+  std::vector<FftRing> rings(nlr);
+  std::vector<double2> arena;
+  std::map<int, int64_t> tw_of_L, chirp_of_N, bhat_of_N;
+  std::vector<int32_t> yrow;
+  int64_t go = 0;
+  for (int lr = 0; lr < nlr; ++lr) {
+    rings[lr].goff_n = go;
+    go += g.nloen[p->my_rings[lr]];
+  }
+  for (int lr = nlr - 1; lr >= 0; --lr) {
+    rings[lr].goff_s = go;
+    go += g.nloen[p->my_rings[lr]];
+  }
+  p->grid_ld = go;
+  const int npairs = (nfld + 1) / 2;
+  const size_t budget_small = 100 * 1024, budget_large = 220 * 1024;
+  std::vector<std::pair<int64_t, FftWork>> wsmall, wlarge;
+  int64_t nfour_local = 0;
+  for (int lr = 0; lr < nlr; ++lr) {
+    const int i = p->my_rings[lr];
+    FftRing& R = rings[lr];
+    R.n = g.nloen[i];
+    R.mcap = g.mcap[i];
+    R.w = p->w[i];
+    nfour_local += 2 * (int64_t)(R.mcap + 1);
+    std::vector<int> rad;
+    int L = 0;
+    bool blue = false;
+    if (fft_choose(R.n, rad, L, blue))
+      return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
+    R.L = L;
+    R.nstage = (int)rad.size();
+    for (int s = 0; s < kMaxStages; ++s) R.radix[s] = s < R.nstage ? (int8_t)rad[s] : 0;
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    const long double pi_ld = 3.14159265358979323846264338327950288L;
+    if (!tw_of_L.count(L)) {
+      tw_of_L[L] = (int64_t)arena.size();
+      for (int k = 0; k < L; ++k) {
+        const long double a = -two_pi * (long double)k / (long double)L;
+        arena.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+      }
+    }
+    R.tw_off = tw_of_L[L];
+    R.chirp_off = R.bhat_off = -1;
+    if (blue) {
+      const int N = R.n;
+      if (!chirp_of_N.count(N)) {
+        std::vector<cld> chirp(N);
+        for (int n = 0; n < N; ++n) {
+          const long long q = ((long long)n * n) % (2LL * N);
+          const long double a = -pi_ld * (long double)q / (long double)N;
+          chirp[n] = cld(cosl(a), sinl(a));
+        }
+        chirp_of_N[N] = (int64_t)arena.size();
+        for (int n = 0; n < N; ++n) arena.push_back(make_double2((double)chirp[n].real(), (double)chirp[n].imag()));
+        std::vector<cld> b(L, cld(0)), bh(L);
+        for (int n = 0; n < N; ++n) {
+          b[n] = std::conj(chirp[n]);
+          if (n) b[L - n] = std::conj(chirp[n]);
+        }
+        dft_rec(b.data(), 1, bh.data(), L);
+        bhat_of_N[N] = (int64_t)arena.size();
+        for (int k = 0; k < L; ++k) {
+          const cld v = bh[k] / (long double)L;
+          arena.push_back(make_double2((double)v.real(), (double)v.imag()));
+        }
+      }
+      R.chirp_off = chirp_of_N[N];
+      R.bhat_off = bhat_of_N[N];
+    }
+    R.yrow_off = (int64_t)yrow.size();
+    for (int m = 0; m <= R.mcap; ++m) {
+      const int s = p->m_owner[m];
+      yrow.push_back((int32_t)(ybase[s][i] + p->lm_of_m[m]));
+    }
+    // field pairs per CTA / sequences per pass: ping + pong buffers of nb
+    // sequences, plus the (M+1) x 2fp staging area of both hemispheres
+    auto smem = [&](int fp, int nb) { return (2 * (size_t)nb * L + 4 * (size_t)(R.mcap + 1) * fp) * sizeof(double2); };
+    auto pick = [&](size_t budget, int& fpo, int& nbo) {
+      for (int fp = std::min(npairs, 64); fp >= 1; --fp) {
+        if (smem(fp, 2 * fp) <= budget) {
+          fpo = fp;
+          nbo = 2 * fp;
+          return true;
+        }
+      }
+      if (smem(1, 1) <= budget) {
+        fpo = 1;
+        nbo = 1;
+        return true;
+      }
+      return false;
+    };
+    int fp = 0, nb = 0;
+    bool small = pick(budget_small, fp, nb);
+    if (!small && !pick(budget_large, fp, nb))
+      return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+    R.fp = fp;
+    R.nb = nb;
+    (small ? p->smem_small : p->smem_large) =
+        std::max(small ? p->smem_small : p->smem_large, smem(fp, nb));
+    for (int fp0 = 0; fp0 < npairs; fp0 += fp) (small ? wsmall : wlarge).push_back({(int64_t)L * R.nstage, {lr, fp0}});
+  }
+  auto bycost = [](const std::pair<int64_t, FftWork>& a, const std::pair<int64_t, FftWork>& b) { return a.first > b.first; };
+  std::stable_sort(wsmall.begin(), wsmall.end(), bycost);
+  std::stable_sort(wlarge.begin(), wlarge.end(), bycost);
+  std::vector<FftWork> work;
+  for (auto& x : wlarge) work.push_back(x.second);
+  for (auto& x : wsmall) work.push_back(x.second);
+  p->nwork_large = (int)wlarge.size();
+  p->nwork_small = (int)wsmall.size();
+  int64_t npts_local = go;
+  p->work_fft = 2.0 * nfld * (8.0 * (double)npts_local + 16.0 * (double)nfour_local);
+  int64_t sent = 0;
+  for (int d = 0; d < P; ++d)
+    if (d != r) sent += p->xrows[d];
+  p->work_a2a = 2.0 * (double)sent * nfld * 32.0;
+
+  // ---- device side
+  int dev = 0;
+  SHT_CUDA_TRY(cudaGetDevice(&dev));
+  SHT_CUDA_TRY(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (int rc = upload(&p->d_mu, p->mu)) return rc;
+  if (int rc = upload(&p->d_sint, p->sint)) return rc;
+  if (int rc = upload(&p->d_lm_m, lm_m)) return rc;
+  if (int rc = upload(&p->d_lm_i0, lm_i0)) return rc;
+  if (int rc = upload(&p->d_lm_kp, lm_kp)) return rc;
+  if (int rc = upload(&p->d_lm_poff, lm_poff)) return rc;
+  if (int rc = upload(&p->d_lm_soff, p->lm_soff)) return rc;
+  if (int rc = upload(&p->d_xbase, xbase)) return rc;
+  if (int rc = upload(&p->d_tiles_inv, ti)) return rc;
+  if (int rc = upload(&p->d_tiles_dir, td)) return rc;
+  if (int rc = upload(&p->d_rings, rings)) return rc;
+  if (int rc = upload(&p->d_work, work)) return rc;
+  if (int rc = upload(&p->d_tw, arena)) return rc;
+  if (int rc = upload(&p->d_yrow, yrow)) return rc;
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
+  const size_t rowb = (size_t)nfld * 4 * sizeof(double);
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->X, std::max<int64_t>(p->xtot, 1) * rowb));
+  if (P == 1) {
+    p->Y = p->X;
+  } else {
+    SHT_CUDA_TRY(cudaMalloc((void**)&p->Y, std::max<int64_t>(p->ytot, 1) * rowb));
+  }
+  for (auto& e : p->ev) SHT_CUDA_TRY(cudaEventCreate(&e));
+  p->have_events = true;
+
+  if (!(p->flags & SHT_FLAG_RECOMPUTE_LEGENDRE)) {
+    SHT_CUDA_TRY(cudaMalloc((void**)&p->d_ptab, std::max<int64_t>(p->ptab_len, 1) * sizeof(double)));
+    SHT_CUDA_TRY(cudaMemset(p->d_ptab, 0, std::max<int64_t>(p->ptab_len, 1) * sizeof(double)));
+    double* dmant = nullptr;
+    int32_t* dexp = nullptr;
+    SHT_CUDA_TRY(cudaMalloc((void**)&dmant, std::max(1, nlm) * (size_t)nh * sizeof(double)));
+    SHT_CUDA_TRY(cudaMalloc((void**)&dexp, std::max(1, nlm) * (size_t)nh * sizeof(int32_t)));
+    SHT_CUDA_TRY(cudaEventRecord(p->ev[8], 0));
+    launch_leg_poly(T, nh, nlm, p->d_lm_m, p->d_lm_i0, p->d_lm_poff, p->d_lm_kp, p->d_mu, p->d_sint, dmant, dexp,
+                    p->d_ptab, 0);
+    SHT_CUDA_TRY(cudaGetLastError());
+    SHT_CUDA_TRY(cudaEventRecord(p->ev[9], 0));
+    SHT_CUDA_TRY(cudaEventSynchronize(p->ev[9]));
+    SHT_CUDA_TRY(cudaEventElapsedTime(&p->setup_ms, p->ev[8], p->ev[9]));
+    cudaFree(dmant);
+    cudaFree(dexp);
+  } else {
+    return fail(SHT_ERR_CONFIG, "SHT_FLAG_RECOMPUTE_LEGENDRE is not available in this build yet");
+  }
+
+  if (P > 1) {
+    if (!nccl_id) return fail(SHT_ERR_CONFIG, "nranks > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    SHT_NCCL_TRY(ncclCommInitRank(&p->comm, P, id, r));
+  }
+  return SHT_OK;
+}
+
+static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles, int* counter) {
+  LegParams lp;
+  lp.T = p->g.T;
+  lp.nh = p->g.nh;
+  lp.nfld = p->nfld;
+  lp.nlm = (int)p->my_m.size();
+  lp.lm_m = p->d_lm_m;
+  lp.lm_i0 = p->d_lm_i0;
+  lp.lm_poff = p->d_lm_poff;
+  lp.lm_kp = p->d_lm_kp;
+  lp.lm_soff = p->d_lm_soff;
+  lp.spec_ld = p->spec_ld;
+  lp.xbase = p->d_xbase;
+  lp.ptab = p->d_ptab;
+  lp.tiles = tiles;
+  lp.ntiles = ntiles;
+  lp.counter = counter;
+  return lp;
+}
+
+static FftParams fft_params(const sht_plan* p) {
+  FftParams fp;
+  fp.nfld = p->nfld;
+  fp.grid_ld = p->grid_ld;
+  fp.rings = p->d_rings;
+  fp.work = p->d_work;
+  fp.nwork = p->nwork_large + p->nwork_small;
+  fp.tw = p->d_tw;
+  fp.yrow = p->d_yrow;
+  return fp;
+}
+
+// Grouped NCCL send/recv in the rotated order of the reference's
+// ROTATED_CONCURRENT schedule (collectives.py:85-86: rank r issues to
+// target (k + r) % P for k = 0..P-1).  The self block is a
+// device copy.  from_x: X -> Y (inverse), else Y -> X (direct).
+static int alltoall(sht_plan* p, bool from_x, cudaStream_t s) {
+  const int P = p->nranks, r = p->rank;
+  const size_t rowd = (size_t)p->nfld * 4;
+  const double* src = from_x ? p->X : p->Y;
+  double* dst = from_x ? p->Y : p->X;
+  const std::vector<int64_t>& soff = from_x ? p->xoff : p->yoff;
+  const std::vector<int64_t>& srows = from_x ? p->xrows : p->yrows;
+  const std::vector<int64_t>& doff = from_x ? p->yoff : p->xoff;
+  const std::vector<int64_t>& drows = from_x ? p->yrows : p->xrows;
+  if (srows[r] > 0)
+    SHT_CUDA_TRY(cudaMemcpyAsync(dst + doff[r] * rowd, src + soff[r] * rowd, srows[r] * rowd * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+  SHT_NCCL_TRY(ncclGroupStart());
+  for (int k = 1; k < P; ++k) {
+    const int to = (r + k) % P, from = (r - k + P) % P;
+    if (srows[to] > 0)
+      SHT_NCCL_TRY(ncclSend(src + soff[to] * rowd, srows[to] * rowd, ncclDouble, to, p->comm, s));
+    if (drows[from] > 0)
+      SHT_NCCL_TRY(ncclRecv(dst + doff[from] * rowd, drows[from] * rowd, ncclDouble, from, p->comm, s));
+  }
+  SHT_NCCL_TRY(ncclGroupEnd());
+  return SHT_OK;
+}
+
+static int check_ptr(const void* q, const char* what) {
+  if (!q) return fail(SHT_ERR_CONFIG, std::string(what) + " is NULL");
+  if (reinterpret_cast<uintptr_t>(q) % 16) return fail(SHT_ERR_CONFIG, std::string(what) + " must be 16-byte aligned");
+  return SHT_OK;
+}
+
+}  // namespace sht
+
+using namespace sht;
+
+extern "C" {
+
+int sht_version(void) { return 100; }
+
+const char* sht_last_error(void) { return g_err.c_str(); }
+
+int sht_gauss_nodes(int ndgl, double* mu, double* sint, double* w) {
+  if (ndgl < 2 || ndgl % 2) return fail(SHT_ERR_CONFIG, "ndgl must be even and >= 2");
+  std::vector<double> a, b, c;
+  gauss_nodes_ld(ndgl, a, b, c);
+  if (mu) std::copy(a.begin(), a.end(), mu);
+  if (sint) std::copy(b.begin(), b.end(), sint);
+  if (w) std::copy(c.begin(), c.end(), w);
+  return SHT_OK;
+}
+
+int sht_partition(int truncation, int ndgl, const int32_t* nloen, int nranks, int32_t* m_owner, int32_t* ring_owner) {
+  Geometry g;
+  if (int rc = make_geometry(truncation, ndgl, nloen, g)) return rc;
+  std::vector<int> mo, ro;
+  if (int rc = build_partition(g, nranks, mo, ro)) return rc;
+  if (m_owner) std::copy(mo.begin(), mo.end(), m_owner);
+  if (ring_owner) std::copy(ro.begin(), ro.end(), ring_owner);
+  return SHT_OK;
+}
+
+int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein) {
+  std::vector<int> rad;
+  int L = 0;
+  bool blue = false;
+  if (n < 1) return fail(SHT_ERR_CONFIG, "ring length must be >= 1");
+  if (fft_choose(n, rad, L, blue)) return fail(SHT_ERR_CONFIG, "no FFT plan for this length");
+  if (radices)
+    for (size_t k = 0; k < rad.size() && k < 32; ++k) radices[k] = rad[k];
+  if (nstages) *nstages = (int32_t)rad.size();
+  if (fft_len) *fft_len = L;
+  if (bluestein) *bluestein = blue ? 1 : 0;
+  return SHT_OK;
+}
+
+int sht_nccl_get_unique_id(void* out128) {
+  if (!out128) return fail(SHT_ERR_CONFIG, "out128 is NULL");
+  ncclUniqueId id;
+  SHT_NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return SHT_OK;
+}
+
+int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, int rank, int nranks,
+                    const void* nccl_unique_id, int flags, sht_plan** out) {
+  if (!out) return fail(SHT_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (nfld < 1) return fail(SHT_ERR_CONFIG, "nfld must be >= 1");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SHT_ERR_CONFIG, "invalid rank / nranks");
+  sht_plan* p = new sht_plan();
+  p->nfld = nfld;
+  p->rank = rank;
+  p->nranks = nranks;
+  p->flags = flags;
+  int rc = make_geometry(truncation, ndgl, nloen, p->g);
+  if (!rc) rc = build_plan(p, nccl_unique_id);
+  if (rc) {
+    const std::string msg = g_err;
+    free_plan(p);
+    g_err = msg;
+    return rc;
+  }
+  *out = p;
+  return SHT_OK;
+}
+
+void sht_plan_destroy(sht_plan* plan) { free_plan(plan); }
+
+int sht_local_layout(const sht_plan* p, int64_t* nspec_re, int64_t* npts, int32_t* m_list, int32_t* n_m,
+                     int32_t* ring_list, int32_t* n_rings) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (nspec_re) *nspec_re = p->spec_ld;
+  if (npts) *npts = p->grid_ld;
+  if (m_list) std::copy(p->my_m.begin(), p->my_m.end(), m_list);
+  if (n_m) *n_m = (int32_t)p->my_m.size();
+  const int nl = (int)p->my_rings.size();
+  if (ring_list) {
+    for (int k = 0; k < nl; ++k) ring_list[k] = p->my_rings[k];
+    for (int k = 0; k < nl; ++k) ring_list[nl + k] = p->g.ndgl - 1 - p->my_rings[nl - 1 - k];
+  }
+  if (n_rings) *n_rings = 2 * nl;
+  return SHT_OK;
+}
+
+int sht_work(const sht_plan* p, double* lf, double* fb, double* ab) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (lf) *lf = p->work_leg;
+  if (fb) *fb = p->work_fft;
+  if (ab) *ab = p->work_a2a;
+  return SHT_OK;
+}
+
+int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (int rc = check_ptr(spec, "spec")) return rc;
+  if (int rc = check_ptr(grid, "grid")) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[0], s));
+  if (p->ntiles_inv) {
+    SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
+    const LegParams lp = leg_params(p, p->d_tiles_inv, p->ntiles_inv, p->d_counter);
+    launch_leg_inv(lp, spec, p->X, std::min(p->nsm, p->ntiles_inv), s);
+    SHT_CUDA_TRY(cudaGetLastError());
+  }
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[1], s));
+  if (p->nranks > 1)
+    if (int rc = alltoall(p, true, s)) return rc;
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[2], s));
+  const FftParams fp = fft_params(p);
+  launch_fft_f2g(fp, 0, p->nwork_large, p->Y, grid, p->smem_large, s);
+  launch_fft_f2g(fp, p->nwork_large, p->nwork_small, p->Y, grid, p->smem_small, s);
+  SHT_CUDA_TRY(cudaGetLastError());
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[3], s));
+  return SHT_OK;
+}
+
+int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (int rc = check_ptr(spec, "spec")) return rc;
+  if (int rc = check_ptr(grid, "grid")) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[4], s));
+  const FftParams fp = fft_params(p);
+  launch_fft_g2f(fp, 0, p->nwork_large, grid, p->Y, p->smem_large, s);
+  launch_fft_g2f(fp, p->nwork_large, p->nwork_small, grid, p->Y, p->smem_small, s);
+  SHT_CUDA_TRY(cudaGetLastError());
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[5], s));
+  if (p->nranks > 1)
+    if (int rc = alltoall(p, false, s)) return rc;
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[6], s));
+  if (p->ntiles_dir) {
+    SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
+    const LegParams lp = leg_params(p, p->d_tiles_dir, p->ntiles_dir, p->d_counter + 1);
+    launch_leg_dir(lp, p->X, spec, std::min(p->nsm, p->ntiles_dir), s);
+    SHT_CUDA_TRY(cudaGetLastError());
+  }
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[7], s));
+  return SHT_OK;
+}
+
+int sht_phase_ms(sht_plan* p, float* ms, int n) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (!(p->flags & SHT_FLAG_PROFILE_PHASES)) return fail(SHT_ERR_CONFIG, "plan was created without SHT_FLAG_PROFILE_PHASES");
+  float v[7] = {p->setup_ms, 0, 0, 0, 0, 0, 0};
+  const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}, {6, 7}};
+  SHT_CUDA_TRY(cudaEventSynchronize(p->ev[7]));
+  SHT_CUDA_TRY(cudaEventSynchronize(p->ev[3]));
+  for (int k = 0; k < 6; ++k) SHT_CUDA_TRY(cudaEventElapsedTime(&v[k + 1], p->ev[pairs[k][0]], p->ev[pairs[k][1]]));
+  for (int k = 0; k < n && k < 7; ++k) ms[k] = v[k];
+  return SHT_OK;
+}
+
+}  // extern "C"

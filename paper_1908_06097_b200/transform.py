@@ -1,0 +1,244 @@
+"""The drop-in transform API: ``SHTransform(truncation, grid, nfld)`` with
+``inv_trans`` (spectral -> grid) and ``dir_trans`` (grid -> spectral).
+
+This is the "CPU reference's Python transform API (setup with truncation,
+grid and field count; inv_trans/dir_trans on field batches)" named by the
+north star (BASELINE.json).  The reference has no such code, so
+the names, argument meaning and error behaviour follow SURVEY.md section 8b;
+``oracle.sht_oracle.SHTransformOracle`` is the CPU restatement with the same
+signature that the tests compare against.
+
+Every call goes through libsht.so (include/sht.h): hand-written sm_100a
+kernels for the Legendre GEMMs (DMMA), the ring FFTs and the Legendre
+polynomial table, plus NCCL for the grid <-> spectral transposition when a
+process group with more than one rank is given.  There is no CPU path.
+
+Array conventions:
+  spectral  float64 [nfld, nspec_local]  m-major, n ascending, re/im interleaved
+            (nspec_local = (T+1)(T+2) on one rank)
+  grid      float64 [nfld, npts_local]   rings north -> south, 2 pi k / NLOEN longitudes
+On more than one rank each rank holds the spectral coefficients of
+``m_list`` and the grid points of ``ring_list`` (see ``local_layout``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigurationError
+
+
+def octahedral_nloen(truncation: int) -> np.ndarray:
+    """NLOEN of the octahedral TCo grid: 4i+16 points on northern ring i (1-based), mirrored south."""
+    T = int(truncation)
+    north = 4 * np.arange(1, T + 2, dtype=np.int32) + 16
+    return np.concatenate([north, north[::-1]])
+
+
+def nspec_real(truncation: int) -> int:
+    T = int(truncation)
+    return (T + 1) * (T + 2)
+
+
+class SHTransform:
+    """Spherical-harmonics transform plan on the current CUDA device.
+
+    Parameters
+    ----------
+    truncation : spectral truncation T (TCo T).
+    grid       : "octahedral" (TCo grid, NDGL = 2(T+1)) or an array of NDGL ring
+                 lengths (north first, north/south symmetric).
+    nfld       : number of fields per batch.
+    group      : torch.distributed process group (NCCL) to shard over, or None
+                 for one GPU.
+    recompute_legendre : recompute P_n^m inside the Legendre GEMMs instead of
+                 storing the table (not in this build: raises ConfigurationError).
+    profile    : record CUDA events around every phase (see ``phase_ms``).
+    """
+
+    def __init__(self, truncation: int, grid="octahedral", nfld: int = 1, *, group=None,
+                 recompute_legendre: bool = False, profile: bool = False, device=None):
+        import torch
+
+        lib = _lib.load()
+        self.T = int(truncation)
+        self.nfld = int(nfld)
+        if self.T < 1:
+            raise ConfigurationError("truncation must be >= 1")
+        if self.nfld < 1:
+            raise ConfigurationError("nfld must be >= 1")
+        if isinstance(grid, str):
+            if grid != "octahedral":
+                raise ConfigurationError(f"unknown grid {grid!r} (use 'octahedral' or an NLOEN array)")
+            self.nloen = octahedral_nloen(self.T)
+            nloen_p = None
+        else:
+            self.nloen = np.ascontiguousarray(np.asarray(grid, dtype=np.int32))
+            if self.nloen.ndim != 1:
+                raise ConfigurationError("grid must be 1-D ring lengths")
+            nloen_p = self.nloen.ctypes.data_as(_lib.i32p)
+        self.ndgl = int(self.nloen.size)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if self.device.type != "cuda":
+            raise ConfigurationError("SHTransform runs on a CUDA device only (no CPU fallback)")
+
+        self.group = group
+        if group is not None:
+            import torch.distributed as dist
+
+            self.rank = dist.get_rank(group)
+            self.nranks = dist.get_world_size(group)
+        else:
+            self.rank, self.nranks = 0, 1
+        uid = None
+        if self.nranks > 1:
+            import torch.distributed as dist
+
+            buf = C.create_string_buffer(128)
+            if self.rank == 0:
+                _lib.check(lib.sht_nccl_get_unique_id(buf))
+            obj = [bytes(buf.raw)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0), group=group)
+            uid = C.create_string_buffer(obj[0], 128)
+        flags = 0
+        if recompute_legendre:
+            flags |= _lib.SHT_FLAG_RECOMPUTE_LEGENDRE
+        if profile:
+            flags |= _lib.SHT_FLAG_PROFILE_PHASES
+        self.profile = bool(profile)
+        plan = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(lib.sht_plan_create(self.T, self.ndgl, nloen_p, self.nfld, self.rank, self.nranks,
+                                           uid, flags, C.byref(plan)))
+        self._plan = plan
+        self._lib = lib
+
+        nspec = C.c_int64()
+        npts = C.c_int64()
+        nm = C.c_int32()
+        nr = C.c_int32()
+        mlist = (C.c_int32 * (self.T + 1))()
+        rlist = (C.c_int32 * self.ndgl)()
+        _lib.check(lib.sht_local_layout(plan, C.byref(nspec), C.byref(npts), mlist, C.byref(nm), rlist, C.byref(nr)))
+        self.nspec_local = int(nspec.value)
+        self.npts_local = int(npts.value)
+        self.m_list = np.array(mlist[: nm.value], dtype=np.int64)
+        self.ring_list = np.array(rlist[: nr.value], dtype=np.int64)
+
+    # ------------------------------------------------------------------ helpers
+    def local_layout(self) -> dict:
+        return {"nspec_local": self.nspec_local, "npts_local": self.npts_local,
+                "m_list": self.m_list.copy(), "ring_list": self.ring_list.copy()}
+
+    def work(self) -> dict:
+        """Algorithmic work of this rank per inverse+direct pair."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        _lib.check(self._lib.sht_work(self._plan, C.byref(a), C.byref(b), C.byref(c)))
+        return {"legendre_flops": a.value, "fft_bytes": b.value, "a2a_bytes": c.value}
+
+    def phase_ms(self) -> dict:
+        """Device times of the last inv_trans + dir_trans (plan created with profile=True)."""
+        v = (C.c_float * 7)()
+        _lib.check(self._lib.sht_phase_ms(self._plan, v, 7))
+        keys = ("legendre_poly_setup", "inv_legendre", "inv_alltoall", "inv_fft", "dir_fft", "dir_alltoall",
+                "dir_legendre")
+        return dict(zip(keys, [float(x) for x in v]))
+
+    def _check(self, x, ncols: int, what: str):
+        import torch
+
+        if not isinstance(x, torch.Tensor):
+            raise ConfigurationError(f"{what} must be a torch.Tensor or numpy array")
+        if x.dtype != torch.float64:
+            raise ConfigurationError(f"{what} must be float64, got {x.dtype}")
+        if x.device != self.device:
+            raise ConfigurationError(f"{what} must live on {self.device}, got {x.device}")
+        if tuple(x.shape) != (self.nfld, ncols):
+            raise ConfigurationError(f"{what} must have shape ({self.nfld}, {ncols}), got {tuple(x.shape)}")
+        if not x.is_contiguous():
+            raise ConfigurationError(f"{what} must be contiguous")
+        if x.data_ptr() % 16:
+            raise ConfigurationError(f"{what} must be 16-byte aligned")
+
+    def _run(self, fn, x, ncols_in: int, ncols_out: int, out, stream):
+        import torch
+
+        host = isinstance(x, np.ndarray)
+        if host:
+            xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
+            xt = xt.to(self.device, non_blocking=True)
+        else:
+            xt = x
+        self._check(xt, ncols_in, "input")
+        if out is None:
+            out = torch.empty((self.nfld, ncols_out), dtype=torch.float64, device=self.device)
+        else:
+            self._check(out, ncols_out, "out")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(fn(self._plan, C.c_void_p(xt.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+        if host:
+            return out.cpu().numpy()
+        return out
+
+    # ------------------------------------------------------------------ API
+    def inv_trans(self, spec, out=None, stream=None):
+        """Spectral [nfld, nspec_local] -> grid [nfld, npts_local] (float64).
+
+        ``spec`` may be a CUDA tensor (result stays on the device, stream-ordered
+        on ``stream`` / the current stream) or a host numpy array (copied in and
+        the result copied back to a numpy array).
+        """
+        return self._run(self._lib.sht_inv_trans, spec, self.nspec_local, self.npts_local, out, stream)
+
+    def dir_trans(self, grid, out=None, stream=None):
+        """Grid [nfld, npts_local] -> spectral [nfld, nspec_local] (float64)."""
+        return self._run(self._lib.sht_dir_trans, grid, self.npts_local, self.nspec_local, out, stream)
+
+    def close(self) -> None:
+        if getattr(self, "_plan", None):
+            self._lib.sht_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gauss_nodes(ndgl: int):
+    """Northern Gaussian nodes (mu, cos(lat), w) as computed by the plan (host-only call)."""
+    lib = _lib.load()
+    nh = int(ndgl) // 2
+    mu, s, w = np.empty(nh), np.empty(nh), np.empty(nh)
+    _lib.check(lib.sht_gauss_nodes(int(ndgl), mu.ctypes.data_as(_lib.f64p), s.ctypes.data_as(_lib.f64p),
+                                   w.ctypes.data_as(_lib.f64p)))
+    return mu, s, w
+
+
+def partition(truncation: int, nranks: int, grid="octahedral"):
+    """(m_owner[T+1], ring_owner[NDGL/2]) the plan uses for ``nranks`` ranks (host-only call)."""
+    lib = _lib.load()
+    T = int(truncation)
+    if isinstance(grid, str):
+        nloen_p, ndgl = None, 2 * (T + 1)
+    else:
+        arr = np.ascontiguousarray(np.asarray(grid, dtype=np.int32))
+        nloen_p, ndgl = arr.ctypes.data_as(_lib.i32p), int(arr.size)
+    mo = np.empty(T + 1, dtype=np.int32)
+    ro = np.empty(ndgl // 2, dtype=np.int32)
+    _lib.check(lib.sht_partition(T, ndgl, nloen_p, int(nranks), mo.ctypes.data_as(_lib.i32p),
+                                 ro.ctypes.data_as(_lib.i32p)))
+    return mo, ro
+
+
+def fft_plan_info(n: int) -> dict:
+    lib = _lib.load()
+    rad = (C.c_int32 * 32)()
+    ns, L, blue = C.c_int32(), C.c_int32(), C.c_int32()
+    _lib.check(lib.sht_fft_plan_info(int(n), rad, C.byref(ns), C.byref(L), C.byref(blue)))
+    return {"radices": list(rad[: ns.value]), "length": L.value, "bluestein": bool(blue.value)}
