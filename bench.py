@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""bench.py -- TCo639 spherical-harmonics inverse+direct transform pair on N B200.
+
+Metric (BASELINE.json): "TCo639 inverse+direct transform ms at 1/2/4/8 B200;
+% FP64/HBM/NVLink roofline".  One step = one inv_trans + dir_trans pair over
+NFLD = 548 synthetic fields (fixed across GPU counts, so
+scaling is strong).  ``value`` = device time per pair (CUDA events around K
+back-to-back pairs on the launching stream, max over ranks); inputs (1.8 GB
+spectral, 7.3 GB grid) are far larger than the 126 MB L2, so no flush is
+needed between steps.  ``e2e`` = the same pair through the public API with
+the spectral input coming from pinned host memory and the spectral result
+going back to it every step.
+
+  python bench.py [--gpus N --steps K --warmup W]            our B200 path
+  python bench.py --impl reference [...]                     CPU oracle arm
+
+Under torchrun (N > 1) every rank drives one GPU through NCCL.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TCo639 inverse+direct transform ms at 1/2/4/8 B200; % FP64/HBM/NVLink roofline"
+UNIT = "ms/pair"
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--truncation", type=int, default=639)
+    ap.add_argument("--nfld", type=int, default=548)
+    ap.add_argument("--cpu-fields", type=int, default=16, help="fields in the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks() -> dict:
+    """Roofline denominators: measured HBM copy (MEASURED_PEAKS.json), measured
+    DMMA issue peak (profiles/r01_probe_fp64.json), measured NVLink peer copy."""
+    hbm, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        try:
+            hbm, hbm_src = float(json.loads(mp.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+        except Exception:
+            pass
+    fp64, fp64_src = 37.14, "profiles/r01_probe_fp64.json (DMMA.8x8x4 issue peak, 1965 MHz)"
+    pf = ROOT / "profiles" / "r01_probe_fp64.json"
+    if pf.exists():
+        try:
+            d = json.loads(pf.read_text())
+            fp64 = max(v for k, v in d.items() if k.startswith("dmma_") and isinstance(v, (int, float)))
+        except Exception:
+            pass
+    return {"fp64_tflops": fp64, "fp64_src": fp64_src, "hbm_gbs": hbm, "hbm_src": hbm_src,
+            "nvlink_gbs": NVLINK_GBS, "nvlink_src": "B200_PROFILING.md measured peer copy per direction"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (rank 0)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict | None:
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[4 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def cpu_oracle_pair_ms(T: int, nfld_sample: int, nfld_full: int, pairs: int = 1, warm: int = 0):
+    """Time the CPU oracle (NumPy/SciPy port, all host threads) on a bounded
+    sample of the workload and scale linearly in the field count."""
+    from oracle.sht_oracle import SHTransformOracle, random_spectral
+
+    o = SHTransformOracle(T, nfld=nfld_sample, workers=os.cpu_count())
+    a = random_spectral(T, nfld_sample)
+    for _ in range(warm):
+        o.dir_trans(o.inv_trans(a))
+    times = []
+    for _ in range(pairs):
+        t0 = time.perf_counter()
+        o.dir_trans(o.inv_trans(a))
+        times.append((time.perf_counter() - t0) * 1e3)
+    per = float(np.mean(times))
+    return per * nfld_full / nfld_sample, per, times
+
+
+def traffic_per_launch(kernel: str):
+    f = ROOT / "profiles" / "traffic.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get(kernel)
+        except Exception:
+            return None
+    return None
+
+
+def run_reference(args):
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    T, nf, ns = args.truncation, args.nfld, args.cpu_fields
+    from oracle.sht_oracle import SHTransformOracle, random_spectral
+
+    o = SHTransformOracle(T, nfld=ns, workers=cores)
+    a = random_spectral(T, ns)
+    for _ in range(args.warmup):
+        o.dir_trans(o.inv_trans(a))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.dir_trans(o.inv_trans(a))
+    per_sample = (time.perf_counter() - t0) * 1e3 / args.steps
+    value = per_sample * nf / ns
+    sample = (f"TCo{T}, {ns} of {nf} fields per inv+dir pair (CPU oracle oracle/sht_oracle.py: NumPy BLAS "
+              f"Legendre GEMMs + scipy.fft ring FFTs, workers={cores}), time scaled x{nf}/{ns} (linear in fields)")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
+                   "grid": "octahedral"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (haloflow) has no transform code (SPEC.md:20); its CPU path is the oracle port",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_06097_b200 import SHTransform
+
+    rank, world, local = dist_setup()
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    group = dist.group.WORLD if world > 1 else None
+    T, nf = args.truncation, args.nfld
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    sh = SHTransform(T, nfld=nf, group=group, profile=True)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(T * 1000 + rank)
+    spec = torch.randn(nf, sh.nspec_local, dtype=torch.float64, device=dev, generator=g) / np.sqrt(2.0)
+    if 0 in sh.m_list:  # Im a_n^0 = 0 (m = 0 is the first local wavenumber when present)
+        spec[:, 1: 2 * (T + 1): 2] = 0.0
+    grid = torch.empty(nf, sh.npts_local, dtype=torch.float64, device=dev)
+    spec2 = torch.empty_like(spec)
+
+    def pair():
+        sh.inv_trans(spec, out=grid)
+        sh.dir_trans(grid, out=spec2)
+
+    for _ in range(args.warmup):
+        pair()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = Clocks(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        pair()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop() if clk else None
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    ph = sh.phase_ms(min(args.steps, 64))
+    work = sh.work()
+    launches = sh.kernel_launches()
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.from_numpy(np.ascontiguousarray(spec.cpu().numpy())).pin_memory()
+        host_out = torch.empty(spec.shape, dtype=torch.float64).pin_memory()
+        dspec = torch.empty_like(spec)
+
+        def e2e_pair():
+            dspec.copy_(host_in, non_blocking=True)
+            sh.inv_trans(dspec, out=grid)
+            sh.dir_trans(grid, out=spec2)
+            host_out.copy_(spec2, non_blocking=True)
+
+        e2e_pair()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record()
+        for _ in range(args.steps):
+            e2e_pair()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        nbytes = spec.numel() * 8
+        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "path": "SHTransform.inv_trans/dir_trans (C-ABI) with pinned-host spectral in/out each pair"}
+
+    pk = peaks()
+    # per-rank phase times (max over ranks = the critical path)
+    leg_ms = max_over_ranks(ph["inv_legendre"] + ph["dir_legendre"], world)
+    fft_ms = max_over_ranks(ph["inv_fft"] + ph["dir_fft"], world)
+    a2a_ms = max_over_ranks(ph["inv_alltoall"] + ph["dir_alltoall"], world)
+    F_leg = max_over_ranks(work["legendre_flops"], world)
+    B_fft = max_over_ranks(work["fft_bytes"], world)
+    B_a2a = max_over_ranks(work["a2a_bytes"], world)
+    t_leg_roof = F_leg / (pk["fp64_tflops"] * 1e12) * 1e3
+    t_fft_roof = B_fft / (pk["hbm_gbs"] * 1e9) * 1e3
+    t_a2a_roof = B_a2a / (pk["nvlink_gbs"] * 1e9) * 1e3 if world > 1 else 0.0
+    t_roof = t_leg_roof + t_fft_roof + t_a2a_roof
+
+    inv_leg, dir_leg = ph["inv_legendre"], ph["dir_legendre"]
+    dom = "leg_inv_kernel" if inv_leg >= dir_leg else "leg_dir_kernel"
+    dom_ms = max(inv_leg, dir_leg)
+    dom_ms = max_over_ranks(dom_ms, world)
+    achieved = (F_leg / 2) / (dom_ms * 1e-3) / 1e12
+    traffic = traffic_per_launch(dom)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        full, per, _ = cpu_oracle_pair_ms(T, args.cpu_fields, nf, pairs=1, warm=0)
+        cpu = {"value": full, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"TCo{T}, {args.cpu_fields} of {nf} fields, one inv+dir pair of the CPU oracle "
+                         f"(NumPy BLAS + scipy.fft, all host threads) = {per:.1f} ms, scaled x{nf}/{args.cpu_fields}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
+                       "grid": "octahedral", "parallelism": f"m/ring-pair sharded x{world}, NCCL all-to-all",
+                       "l2": "inputs larger than L2 (spectral 1.8 GB, grid 7.3 GB per pair at 1 GPU)"},
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": pk["fp64_tflops"],
+                         "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"], "traffic": traffic,
+                         "peak_src": pk["fp64_src"],
+                         "per_launch": f"{F_leg / 2:.4e} FP64 flop (4*NFLD*sum_m NDGLU(m)(T-m+1) per direction)"},
+            "combined_roofline": {
+                "t_roof_ms": t_roof, "frac": t_roof / ms, "legendre_roof_ms": t_leg_roof,
+                "fft_roof_ms": t_fft_roof, "a2a_roof_ms": t_a2a_roof,
+                "phases_ms": {"legendre": leg_ms, "fft": fft_ms, "alltoall": a2a_ms},
+                "phase_frac": {"legendre_fp64": t_leg_roof / leg_ms if leg_ms else None,
+                               "fft_hbm": t_fft_roof / fft_ms if fft_ms else None,
+                               "alltoall_nvlink": (t_a2a_roof / a2a_ms) if a2a_ms else None},
+                "peaks": pk,
+            },
+            "phases_ms": ph,
+            "setup_s": setup_s,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -89,9 +89,16 @@ int sht_local_layout(const sht_plan* plan, int64_t* nspec_re, int64_t* npts, int
  * Synchronises on the recorded events. */
 int sht_phase_ms(sht_plan* plan, float* ms, int n);
 
+/* Same, averaged over the last `npairs` (<= 64) inverse+direct pairs.  A pair
+ * is an sht_inv_trans followed by an sht_dir_trans. */
+int sht_phase_ms_avg(sht_plan* plan, int npairs, float* ms, int n);
+
 /* Algorithmic work of this rank per inverse+direct pair:
  * Legendre flops, FFT HBM bytes, all-to-all bytes sent to other ranks. */
 int sht_work(const sht_plan* plan, double* legendre_flops, double* fft_bytes, double* a2a_bytes);
+
+/* Number of libsht kernel launches one inverse+direct pair issues. */
+int sht_kernel_launches(const sht_plan* plan, int* per_pair);
 
 /* 128-byte NCCL unique id (call on rank 0 only). */
 int sht_nccl_get_unique_id(void* out128);
@@ -111,6 +118,17 @@ int sht_gauss_nodes(int ndgl, double* mu, double* sint, double* w);
  * its southern mirror).  nloen may be NULL (octahedral). */
 int sht_partition(int truncation, int ndgl, const int32_t* nloen, int nranks, int32_t* m_owner,
                   int32_t* ring_owner);
+
+/* Size matrix of the grid <-> spectral transposition for `nranks` ranks, in
+ * Fourier rows (one row = nfld x 4 doubles = 32*nfld bytes): rows[r*nranks + d]
+ * = rows rank r sends to rank d in the inverse transform (the direct transform
+ * sends the transpose).  This is the `sizes` argument of the reference's
+ * collectives.build_alltoall (collectives.py:96) for this data path. */
+int sht_alltoall_rows(int truncation, int ndgl, const int32_t* nloen, int nranks, int64_t* rows);
+
+/* Issue order of rank `rank`'s transfers: peers[k] = (rank + k) % nranks, the
+ * reference's ROTATED_CONCURRENT order (collectives.py:85-86). */
+int sht_alltoall_order(int nranks, int rank, int32_t* peers);
 
 /* FFT plan chosen for a ring of n points: number of radix stages written to
  * radices (capacity 32), transform length L (n, or the Bluestein length) and

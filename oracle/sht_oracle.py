@@ -41,7 +41,10 @@ reference transform exists" is what DESIGN.md states.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
+import scipy.fft as _sfft
 
 __all__ = [
     "octahedral_nloen",
@@ -249,8 +252,9 @@ class SHTransformOracle:
     (north first, north/south symmetric).
     """
 
-    def __init__(self, truncation: int, grid="octahedral", nfld: int = 1):
+    def __init__(self, truncation: int, grid="octahedral", nfld: int = 1, workers: int | None = None):
         T = int(truncation)
+        self.workers = int(workers) if workers else (os.cpu_count() or 1)
         if T < 1:
             raise ValueError("truncation must be >= 1")
         self.T = T
@@ -278,18 +282,25 @@ class SHTransformOracle:
 
     # -- helpers ---------------------------------------------------------------
     def _fourier_inv(self, spec: np.ndarray):
-        """Legendre synthesis: Fourier coefficients per ring, list of [nfld, M_j+1] complex."""
-        T, nh = self.T, self.nh
-        a = spec[:, 0::2] + 1j * spec[:, 1::2]
-        four = [np.zeros((self.nfld, int(self.mcap[j]) + 1), dtype=np.complex128) for j in range(self.ndgl)]
+        """Legendre synthesis: Fourier coefficients per ring, list of [nfld, M_j+1] complex.
+
+        Per m the S (even n-m) and A (odd n-m) sums are real GEMMs over the
+        re/im-interleaved coefficients; F_north = S + A, F_south = S - A.
+        """
+        T, nh, nf = self.T, self.nh, self.nfld
+        four = [np.zeros((nf, int(self.mcap[j]) + 1), dtype=np.complex128) for j in range(self.ndgl)]
         for m in range(T + 1):
             i0, P = self.tables[m]
             if i0 >= nh:
                 continue
-            am = a[:, self.soff[m]: self.soff[m + 1]]          # [nfld, K]
-            S = P[:, 0::2] @ am[:, 0::2].T                      # [rings, nfld]
-            A = P[:, 1::2] @ am[:, 1::2].T
-            fn, fs = S + A, S - A
+            K = T - m + 1
+            am = spec[:, 2 * self.soff[m]: 2 * self.soff[m + 1]].reshape(nf, K, 2)
+            bs = am[:, 0::2, :].transpose(1, 0, 2).reshape(-1, 2 * nf)       # [K_S, nfld*2]
+            ba = am[:, 1::2, :].transpose(1, 0, 2).reshape(-1, 2 * nf)
+            S = (P[:, 0::2] @ bs).reshape(-1, nf, 2)                          # [rings, nfld, 2]
+            A = (P[:, 1::2] @ ba).reshape(-1, nf, 2)
+            fn = (S + A)[..., 0] + 1j * (S + A)[..., 1]
+            fs = (S - A)[..., 0] + 1j * (S - A)[..., 1]
             for r, i in enumerate(range(i0, nh)):
                 four[i][:, m] = fn[r]
                 four[self.ndgl - 1 - i][:, m] = fs[r]
@@ -304,7 +315,7 @@ class SHTransformOracle:
             n = int(self.nloen[j])
             c = np.zeros((self.nfld, n // 2 + 1), dtype=np.complex128)
             c[:, : four[j].shape[1]] = four[j]
-            grid[:, self.roff[j]: self.roff[j + 1]] = np.fft.irfft(c, n=n, axis=1) * n
+            grid[:, self.roff[j]: self.roff[j + 1]] = _sfft.irfft(c, n=n, axis=1, workers=self.workers) * n
         return grid
 
     def fourier_dir(self, grid: np.ndarray):
@@ -312,7 +323,7 @@ class SHTransformOracle:
         out = []
         for j in range(self.ndgl):
             n = int(self.nloen[j])
-            z = np.fft.rfft(grid[:, self.roff[j]: self.roff[j + 1]], axis=1) / n
+            z = _sfft.rfft(grid[:, self.roff[j]: self.roff[j + 1]], axis=1, workers=self.workers) / n
             out.append(z[:, : int(self.mcap[j]) + 1])
         return out
 
@@ -320,21 +331,21 @@ class SHTransformOracle:
         """Grid [nfld, NPTS] -> spectral [nfld, (T+1)(T+2)] (float64)."""
         grid = np.asarray(grid, dtype=np.float64).reshape(self.nfld, self.npts)
         four = self.fourier_dir(grid)
-        T, nh = self.T, self.nh
-        a = np.zeros((self.nfld, self.nspec // 2), dtype=np.complex128)
+        T, nh, nf = self.T, self.nh, self.nfld
+        spec = np.zeros((nf, self.nspec))
         for m in range(T + 1):
             i0, P = self.tables[m]
             if i0 >= nh:
                 continue
+            K = T - m + 1
             fn = np.stack([four[i][:, m] for i in range(i0, nh)])                 # [rings, nfld]
             fs = np.stack([four[self.ndgl - 1 - i][:, m] for i in range(i0, nh)])
             w = self.w[i0:nh, None]
             gs, ga = w * (fn + fs), w * (fn - fs)
-            out = np.empty((T - m + 1, self.nfld), dtype=np.complex128)
-            out[0::2] = P[:, 0::2].T @ gs
-            out[1::2] = P[:, 1::2].T @ ga
-            a[:, self.soff[m]: self.soff[m + 1]] = out.T
-        spec = np.empty((self.nfld, self.nspec))
-        spec[:, 0::2] = a.real
-        spec[:, 1::2] = a.imag
+            gs = np.stack([gs.real, gs.imag], axis=-1).reshape(-1, 2 * nf)        # [rings, nfld*2]
+            ga = np.stack([ga.real, ga.imag], axis=-1).reshape(-1, 2 * nf)
+            out = np.empty((K, nf, 2))
+            out[0::2] = (P[:, 0::2].T @ gs).reshape(-1, nf, 2)
+            out[1::2] = (P[:, 1::2].T @ ga).reshape(-1, nf, 2)
+            spec[:, 2 * self.soff[m]: 2 * self.soff[m + 1]] = out.transpose(1, 0, 2).reshape(nf, 2 * K)
         return spec

@@ -1,0 +1,124 @@
+"""CPU restatement of the distributed data path -- TEST INFRASTRUCTURE ONLY.
+
+Restates, independently of libsht's C++ plan (paper_1908_06097_b200/csrc/
+sht_plan.cu), how the transform is sharded over P ranks and how the
+grid <-> spectral transposition moves Fourier rows, so the CPU test-suite can
+check the partition, the size matrix and the pack/unpack index math without a
+GPU, in process (the reference's oracle-equivalence pattern,
+/root/reference/pkg/tests/test_acceptance.py:60-80: a P-rank run must equal
+the 1-rank oracle) and across real processes over gloo.
+
+* Ownership: snake (boustrophedon) dealing of the zonal wavenumbers m and of
+  the northern ring pairs i over the ranks.
+* Issue order: rank r sends to (r + k) % P for k = 0..P-1, the reference's
+  ROTATED_CONCURRENT schedule (/root/reference/pkg/src/haloflow/
+  collectives.py:85-86).
+* Fourier rows: one row per (ring pair i, m <= M_i) holding nfld x
+  (S.re, S.im, A.re, A.im); rank r's send block for rank d lists d's rings
+  ascending and, per ring, r's wavenumbers ascending.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .sht_oracle import SHTransformOracle
+
+
+def snake(n: int, P: int) -> np.ndarray:
+    k = np.arange(n)
+    blk, pos = k // P, k % P
+    return np.where(blk % 2 == 0, pos, P - 1 - pos).astype(np.int64)
+
+
+class Layout:
+    """Ownership and row layout of a P-rank plan (restated)."""
+
+    def __init__(self, o: SHTransformOracle, P: int):
+        self.o, self.P = o, P
+        self.m_owner = snake(o.T + 1, P)
+        self.ring_owner = snake(o.nh, P)
+        self.M = [np.flatnonzero(self.m_owner == r) for r in range(P)]
+        self.R = [np.flatnonzero(self.ring_owner == r) for r in range(P)]
+        self.mcap = o.mcap[: o.nh]
+
+    def rows(self) -> np.ndarray:
+        """rows[r, d]: Fourier rows r sends to d in the inverse transposition."""
+        P = self.P
+        out = np.zeros((P, P), dtype=np.int64)
+        for r in range(P):
+            for d in range(P):
+                out[r, d] = sum(int(np.sum(self.M[r] <= self.mcap[i])) for i in self.R[d])
+        return out
+
+    def local_spec(self, spec: np.ndarray, r: int) -> np.ndarray:
+        soff = self.o.soff
+        return np.concatenate([spec[:, 2 * soff[m]: 2 * soff[m + 1]] for m in self.M[r]], axis=1)
+
+    def local_rings(self, r: int) -> list:
+        """Global ring indices in local storage order (north asc, then south mirrors)."""
+        north = list(self.R[r])
+        return north + [self.o.ndgl - 1 - i for i in reversed(north)]
+
+    def local_grid(self, grid: np.ndarray, r: int) -> np.ndarray:
+        roff = self.o.roff
+        return np.concatenate([grid[:, roff[j]: roff[j + 1]] for j in self.local_rings(r)], axis=1)
+
+    # -- inverse transform, split at the transposition -------------------------
+    def pack_inv(self, spec_local: np.ndarray, r: int) -> list:
+        """Legendre side of rank r: per destination d, the flat float64 send block."""
+        o, T, nf = self.o, self.o.T, self.o.nfld
+        rows = {}  # (i, m) -> [nfld, 4]
+        off = 0
+        for m in self.M[r]:
+            K = T - m + 1
+            i0, P = o.tables[m]
+            am = spec_local[:, 2 * off: 2 * (off + K)].reshape(nf, K, 2)
+            off += K
+            if i0 >= o.nh:
+                continue
+            bs = am[:, 0::2, :].transpose(1, 0, 2).reshape(-1, 2 * nf)
+            ba = am[:, 1::2, :].transpose(1, 0, 2).reshape(-1, 2 * nf)
+            S = (P[:, 0::2] @ bs).reshape(-1, nf, 2)
+            A = (P[:, 1::2] @ ba).reshape(-1, nf, 2)
+            for k, i in enumerate(range(i0, o.nh)):
+                rows[(i, m)] = np.concatenate([S[k], A[k]], axis=1)  # S.re S.im A.re A.im
+        blocks = []
+        for d in range(self.P):
+            parts = [rows[(i, m)] for i in self.R[d] for m in self.M[r] if m <= self.mcap[i]]
+            blocks.append(np.concatenate([p.reshape(-1) for p in parts]) if parts else np.zeros(0))
+        return blocks
+
+    def unpack_inv(self, recv: list, r: int) -> np.ndarray:
+        """FFT side of rank r: receive blocks (per source s) -> local grid."""
+        o, nf = self.o, self.o.nfld
+        four = {}
+        for s in range(self.P):
+            buf = recv[s].reshape(-1, nf, 4)
+            k = 0
+            for i in self.R[r]:
+                for m in self.M[s]:
+                    if m <= self.mcap[i]:
+                        four[(i, m)] = buf[k]
+                        k += 1
+            assert k == buf.shape[0]
+        cols = []
+        for j in self.local_rings(r):
+            i = j if j < o.nh else o.ndgl - 1 - j
+            sgn = 1.0 if j < o.nh else -1.0
+            M = int(self.mcap[i])
+            n = int(o.nloen[j])
+            c = np.zeros((nf, n // 2 + 1), dtype=np.complex128)
+            for m in range(M + 1):
+                row = four[(i, m)]
+                f = row[:, 0:2] + sgn * row[:, 2:4]
+                c[:, m] = f[:, 0] + 1j * f[:, 1]
+            cols.append(np.fft.irfft(c, n=n, axis=1) * n)
+        return np.concatenate(cols, axis=1)
+
+
+def emulate_inv(o: SHTransformOracle, spec: np.ndarray, P: int):
+    """In-process P-rank inverse transform; returns the list of local grids."""
+    lay = Layout(o, P)
+    send = [lay.pack_inv(lay.local_spec(spec, r), r) for r in range(P)]
+    return [lay.unpack_inv([send[s][r] for s in range(P)], r) for r in range(P)], lay

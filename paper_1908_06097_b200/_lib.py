@@ -25,8 +25,8 @@ SHT_FLAG_PROFILE_PHASES = 2
 # every symbol include/sht.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "sht_version", "sht_plan_create", "sht_inv_trans", "sht_dir_trans", "sht_local_layout",
-    "sht_phase_ms", "sht_work", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
-    "sht_gauss_nodes", "sht_partition", "sht_fft_plan_info",
+    "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
+    "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
 )
 
 _lib = None
@@ -56,12 +56,16 @@ def load() -> C.CDLL:
     lib.sht_dir_trans.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.sht_local_layout.argtypes = [C.c_void_p, i64p, i64p, i32p, i32p, i32p, i32p]
     lib.sht_phase_ms.argtypes = [C.c_void_p, f32p, C.c_int]
+    lib.sht_phase_ms_avg.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int]
     lib.sht_work.argtypes = [C.c_void_p, f64p, f64p, f64p]
+    lib.sht_kernel_launches.argtypes = [C.c_void_p, i32p]
     lib.sht_nccl_get_unique_id.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.restype = None
     lib.sht_gauss_nodes.argtypes = [C.c_int, f64p, f64p, f64p]
     lib.sht_partition.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i32p, i32p]
+    lib.sht_alltoall_rows.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i64p]
+    lib.sht_alltoall_order.argtypes = [C.c_int, C.c_int, i32p]
     lib.sht_fft_plan_info.argtypes = [C.c_int, i32p, i32p, i32p, i32p]
     for name in EXPORTS:
         if name not in ("sht_version", "sht_last_error", "sht_plan_destroy"):

@@ -194,7 +194,11 @@ struct sht_plan {
   int32_t* d_yrow = nullptr;
   ncclComm_t comm = nullptr;
   bool have_events = false;
-  cudaEvent_t ev[10];
+  cudaEvent_t ev[10];                      // ev[8], ev[9]: set-up timing
+  static constexpr int kHist = 64;         // per-pair phase events of the last kHist pairs
+  cudaEvent_t hist[kHist][8];
+  bool hist_inv[kHist] = {};               // set k holds the events of an inverse transform
+  int hist_cur = 0, hist_done = 0;
   float setup_ms = 0.f;
 };
 
@@ -207,8 +211,11 @@ static void free_plan(sht_plan* p) {
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
   for (void* q : ptrs)
     if (q) cudaFree(q);
-  if (p->have_events)
+  if (p->have_events) {
     for (auto& e : p->ev) cudaEventDestroy(e);
+    for (auto& set : p->hist)
+      for (auto& e : set) cudaEventDestroy(e);
+  }
   if (p->comm) ncclCommDestroy(p->comm);
   delete p;
 }
@@ -477,6 +484,8 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     SHT_CUDA_TRY(cudaMalloc((void**)&p->Y, std::max<int64_t>(p->ytot, 1) * rowb));
   }
   for (auto& e : p->ev) SHT_CUDA_TRY(cudaEventCreate(&e));
+  for (auto& set : p->hist)
+    for (auto& e : set) SHT_CUDA_TRY(cudaEventCreate(&e));
   p->have_events = true;
 
   if (!(p->flags & SHT_FLAG_RECOMPUTE_LEGENDRE)) {
@@ -604,6 +613,30 @@ int sht_partition(int truncation, int ndgl, const int32_t* nloen, int nranks, in
   return SHT_OK;
 }
 
+int sht_alltoall_rows(int truncation, int ndgl, const int32_t* nloen, int nranks, int64_t* rows) {
+  Geometry g;
+  if (int rc = make_geometry(truncation, ndgl, nloen, g)) return rc;
+  std::vector<int> mo, ro;
+  if (int rc = build_partition(g, nranks, mo, ro)) return rc;
+  const int P = nranks;
+  // rows[r][d] = sum over rings i of d of #{m of r : m <= M_i}
+  std::vector<std::vector<int64_t>> cnt(P, std::vector<int64_t>(g.nh, 0));
+  for (int i = 0; i < g.nh; ++i)
+    for (int m = 0; m <= std::min(g.T, g.mcap[i]); ++m) cnt[mo[m]][i] += 1;
+  if (rows) {
+    for (int k = 0; k < P * P; ++k) rows[k] = 0;
+    for (int i = 0; i < g.nh; ++i)
+      for (int r = 0; r < P; ++r) rows[(int64_t)r * P + ro[i]] += cnt[r][i];
+  }
+  return SHT_OK;
+}
+
+int sht_alltoall_order(int nranks, int rank, int32_t* peers) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SHT_ERR_CONFIG, "invalid rank / nranks");
+  for (int k = 0; k < nranks; ++k) peers[k] = (rank + k) % nranks;  // collectives.py:85-86
+  return SHT_OK;
+}
+
 int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein) {
   std::vector<int> rad;
   int L = 0;
@@ -681,22 +714,25 @@ int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
   if (int rc = check_ptr(grid, "grid")) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[0], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][0], s));
   if (p->ntiles_inv) {
     SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
     const LegParams lp = leg_params(p, p->d_tiles_inv, p->ntiles_inv, p->d_counter);
     launch_leg_inv(lp, spec, p->X, std::min(p->nsm, p->ntiles_inv), s);
     SHT_CUDA_TRY(cudaGetLastError());
   }
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[1], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][1], s));
   if (p->nranks > 1)
     if (int rc = alltoall(p, true, s)) return rc;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[2], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][2], s));
   const FftParams fp = fft_params(p);
   launch_fft_f2g(fp, 0, p->nwork_large, p->Y, grid, p->smem_large, s);
   launch_fft_f2g(fp, p->nwork_large, p->nwork_small, p->Y, grid, p->smem_small, s);
   SHT_CUDA_TRY(cudaGetLastError());
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[3], s));
+  if (prof) {
+    SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][3], s));
+    p->hist_inv[p->hist_cur] = true;
+  }
   return SHT_OK;
 }
 
@@ -706,34 +742,57 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   if (int rc = check_ptr(grid, "grid")) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[4], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][4], s));
   const FftParams fp = fft_params(p);
   launch_fft_g2f(fp, 0, p->nwork_large, grid, p->Y, p->smem_large, s);
   launch_fft_g2f(fp, p->nwork_large, p->nwork_small, grid, p->Y, p->smem_small, s);
   SHT_CUDA_TRY(cudaGetLastError());
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[5], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][5], s));
   if (p->nranks > 1)
     if (int rc = alltoall(p, false, s)) return rc;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[6], s));
+  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][6], s));
   if (p->ntiles_dir) {
     SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
     const LegParams lp = leg_params(p, p->d_tiles_dir, p->ntiles_dir, p->d_counter + 1);
     launch_leg_dir(lp, p->X, spec, std::min(p->nsm, p->ntiles_dir), s);
     SHT_CUDA_TRY(cudaGetLastError());
   }
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->ev[7], s));
+  if (prof) {
+    SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][7], s));
+    p->hist_cur = (p->hist_cur + 1) % sht_plan::kHist;
+    p->hist_inv[p->hist_cur] = false;
+    p->hist_done = std::min(p->hist_done + 1, sht_plan::kHist);
+  }
   return SHT_OK;
 }
 
-int sht_phase_ms(sht_plan* p, float* ms, int n) {
+int sht_kernel_launches(const sht_plan* p, int* per_pair) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  const int fft = (p->nwork_large > 0) + (p->nwork_small > 0);
+  if (per_pair) *per_pair = (p->ntiles_inv > 0) + (p->ntiles_dir > 0) + 2 * fft;
+  return SHT_OK;
+}
+
+int sht_phase_ms(sht_plan* p, float* ms, int n) { return sht_phase_ms_avg(p, 1, ms, n); }
+
+int sht_phase_ms_avg(sht_plan* p, int npairs, float* ms, int n) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   if (!(p->flags & SHT_FLAG_PROFILE_PHASES)) return fail(SHT_ERR_CONFIG, "plan was created without SHT_FLAG_PROFILE_PHASES");
-  float v[7] = {p->setup_ms, 0, 0, 0, 0, 0, 0};
+  if (npairs < 1 || npairs > p->hist_done) return fail(SHT_ERR_CONFIG, "npairs must be in [1, completed pairs <= 64]");
+  double v[7] = {p->setup_ms, 0, 0, 0, 0, 0, 0};
   const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}, {6, 7}};
-  SHT_CUDA_TRY(cudaEventSynchronize(p->ev[7]));
-  SHT_CUDA_TRY(cudaEventSynchronize(p->ev[3]));
-  for (int k = 0; k < 6; ++k) SHT_CUDA_TRY(cudaEventElapsedTime(&v[k + 1], p->ev[pairs[k][0]], p->ev[pairs[k][1]]));
-  for (int k = 0; k < n && k < 7; ++k) ms[k] = v[k];
+  for (int q = 1; q <= npairs; ++q) {
+    const int slot = (p->hist_cur - q + sht_plan::kHist) % sht_plan::kHist;
+    cudaEvent_t* e = p->hist[slot];
+    SHT_CUDA_TRY(cudaEventSynchronize(e[7]));
+    for (int k = 0; k < 6; ++k) {
+      if (k < 3 && !p->hist_inv[slot]) continue;  // a direct transform without a preceding inverse
+      float t = 0.f;
+      SHT_CUDA_TRY(cudaEventElapsedTime(&t, e[pairs[k][0]], e[pairs[k][1]]));
+      v[k + 1] += t / npairs;
+    }
+  }
+  for (int k = 0; k < n && k < 7; ++k) ms[k] = (float)v[k];
   return SHT_OK;
 }
 

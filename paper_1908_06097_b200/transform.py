@@ -140,10 +140,17 @@ class SHTransform:
         _lib.check(self._lib.sht_work(self._plan, C.byref(a), C.byref(b), C.byref(c)))
         return {"legendre_flops": a.value, "fft_bytes": b.value, "a2a_bytes": c.value}
 
-    def phase_ms(self) -> dict:
-        """Device times of the last inv_trans + dir_trans (plan created with profile=True)."""
+    def kernel_launches(self) -> int:
+        """libsht kernel launches issued by one inv_trans + dir_trans pair."""
+        n = C.c_int32()
+        _lib.check(self._lib.sht_kernel_launches(self._plan, C.byref(n)))
+        return int(n.value)
+
+    def phase_ms(self, npairs: int = 1) -> dict:
+        """Device times (ms) per phase, averaged over the last ``npairs`` (<= 64)
+        inv_trans + dir_trans pairs (plan created with profile=True)."""
         v = (C.c_float * 7)()
-        _lib.check(self._lib.sht_phase_ms(self._plan, v, 7))
+        _lib.check(self._lib.sht_phase_ms_avg(self._plan, int(npairs), v, 7))
         keys = ("legendre_poly_setup", "inv_legendre", "inv_alltoall", "inv_fft", "dir_fft", "dir_alltoall",
                 "dir_legendre")
         return dict(zip(keys, [float(x) for x in v]))
@@ -234,6 +241,36 @@ def partition(truncation: int, nranks: int, grid="octahedral"):
     _lib.check(lib.sht_partition(T, ndgl, nloen_p, int(nranks), mo.ctypes.data_as(_lib.i32p),
                                  ro.ctypes.data_as(_lib.i32p)))
     return mo, ro
+
+
+def _nloen_arg(truncation: int, grid):
+    T = int(truncation)
+    if isinstance(grid, str):
+        return None, 2 * (T + 1), None
+    arr = np.ascontiguousarray(np.asarray(grid, dtype=np.int32))
+    return arr.ctypes.data_as(_lib.i32p), int(arr.size), arr
+
+
+def alltoall_rows(truncation: int, nranks: int, grid="octahedral") -> np.ndarray:
+    """[P, P] Fourier rows rank r sends to rank d in the inverse transposition (host-only call).
+
+    Multiply by 32 * nfld for bytes: this is the ``sizes`` matrix of the
+    reference's ``collectives.build_alltoall`` (collectives.py:96) for this path.
+    """
+    lib = _lib.load()
+    ptr, ndgl, _keep = _nloen_arg(truncation, grid)
+    P = int(nranks)
+    rows = np.empty(P * P, dtype=np.int64)
+    _lib.check(lib.sht_alltoall_rows(int(truncation), ndgl, ptr, P, rows.ctypes.data_as(_lib.i64p)))
+    return rows.reshape(P, P)
+
+
+def alltoall_order(nranks: int, rank: int) -> list:
+    """Peers in the order rank ``rank`` issues its transfers (rotated, collectives.py:85-86)."""
+    lib = _lib.load()
+    out = np.empty(int(nranks), dtype=np.int32)
+    _lib.check(lib.sht_alltoall_order(int(nranks), int(rank), out.ctypes.data_as(_lib.i32p)))
+    return [int(x) for x in out]
 
 
 def fft_plan_info(n: int) -> dict:

@@ -1,0 +1,132 @@
+"""The C-ABI boundary: libsht.so builds, loads, exports every symbol of
+include/sht.h, and its host-only helpers agree with the oracle bit for bit.
+No GPU compute is called here."""
+
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.sht_oracle import gauss_nodes as oracle_nodes
+from oracle.transposition import Layout, snake
+from oracle.sht_oracle import SHTransformOracle
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "sht.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(sht_\w+)\s*\(", text, re.M)))
+
+
+def test_exports_every_header_symbol(lib):
+    from paper_1908_06097_b200 import _lib
+
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(_lib.EXPORTS) == syms
+    assert lib.sht_version() >= 100
+
+
+def test_library_is_sm100a(lib):
+    import subprocess
+
+    from paper_1908_06097_b200 import _lib
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "DMMA.8x8x4" in sass            # FP64 tensor-core Legendre GEMMs
+    assert "LDGSTS" in sass                # cp.async operand staging
+
+
+@pytest.mark.parametrize("ndgl", [2, 160, 1280, 2560])
+def test_gauss_nodes_bit_identical(lib, ndgl):
+    from paper_1908_06097_b200 import gauss_nodes
+
+    a = gauss_nodes(ndgl)
+    b = oracle_nodes(ndgl)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("T,P", [(79, 1), (79, 2), (639, 4), (639, 8), (20, 3)])
+def test_partition_matches_restatement(lib, T, P):
+    from paper_1908_06097_b200 import partition
+
+    mo, ro = partition(T, P)
+    assert np.array_equal(mo, snake(T + 1, P))
+    assert np.array_equal(ro, snake(T + 1, P))
+    # balance: Legendre work within 2% and grid points within 2% across ranks at TCo639
+    if T == 639:
+        nloen = 4 * np.arange(1, T + 2) + 16
+        mc = np.minimum(T, (nloen - 1) // 2)
+        ndglu = np.array([(mc >= m).sum() for m in range(T + 1)])
+        work = ndglu * (T - np.arange(T + 1) + 1)
+        wr = np.bincount(mo, weights=work, minlength=P)
+        pr = np.bincount(ro, weights=nloen, minlength=P)
+        assert wr.max() / wr.mean() < 1.02 and pr.max() / pr.mean() < 1.02
+
+
+@pytest.mark.parametrize("T,P", [(15, 2), (79, 3), (639, 8)])
+def test_alltoall_rows_match_restatement(lib, T, P):
+    from paper_1908_06097_b200 import alltoall_rows
+
+    o = SHTransformOracle(T, nfld=1) if T < 100 else None
+    rows = alltoall_rows(T, P)
+    if o is not None:
+        assert np.array_equal(rows, Layout(o, P).rows())
+    nloen = 4 * np.arange(1, T + 2) + 16
+    assert rows.sum() == int(np.sum(np.minimum(T, (nloen - 1) // 2) + 1))   # every (ring pair, m) once
+
+
+def test_alltoall_order_is_reference_rotated_schedule(lib):
+    """Issue order == haloflow build_alltoall(ROTATED_CONCURRENT) (collectives.py:85-86),
+    pinned by tests/golden/schedules.json generated from the reference itself."""
+    from paper_1908_06097_b200 import alltoall_order
+
+    gold = json.loads((ROOT / "tests" / "golden" / "schedules.json").read_text())["rotated_order"]
+    for P, flows in gold.items():
+        P = int(P)
+        ours = [[r, d] for r in range(P) for d in alltoall_order(P, r)]
+        assert ours == flows
+
+
+def test_size_matrix_golden(lib):
+    from paper_1908_06097_b200 import alltoall_rows
+
+    gold = json.loads((ROOT / "tests" / "golden" / "schedules.json").read_text())["tco639"]
+    for P, d in gold.items():
+        assert alltoall_rows(639, int(P)).tolist() == d["rows"]
+        ms = d["makespan_s"]
+        assert ms["rotated_concurrent"] <= min(ms.values()) + 1e-12   # the paper's winner
+
+
+def test_fft_plans(lib):
+    from paper_1908_06097_b200 import fft_plan_info
+
+    assert fft_plan_info(20) == {"radices": [4, 5], "length": 20, "bluestein": False}
+    big = fft_plan_info(2576)                      # 2576 = 2^4 * 7 * 23 -> Bluestein
+    assert big["bluestein"] and big["length"] >= 2 * 2576 - 1
+    assert int(np.prod(big["radices"])) == big["length"]
+    for n in range(20, 2600, 4):
+        info = fft_plan_info(n)
+        assert int(np.prod(info["radices"])) == info["length"]
+        assert info["length"] == n or info["bluestein"]
+
+
+def test_errors_map_to_reference_classes(lib):
+    from paper_1908_06097_b200 import ConfigurationError, alltoall_order, partition
+
+    with pytest.raises(ConfigurationError):
+        partition(0, 2)
+    with pytest.raises(ConfigurationError):
+        partition(10, 0)
+    with pytest.raises(ConfigurationError):
+        partition(10, 2, grid=np.array([20, 24, 28, 20]))     # not symmetric
+    with pytest.raises(ConfigurationError):
+        alltoall_order(2, 5)

@@ -1,0 +1,166 @@
+"""GPU parity: SHTransform (libsht.so, sm_100a kernels) vs the CPU oracle and
+the golden fixtures.  Bar (BASELINE.json north star): per field
+max|x - x_ref| / max|x_ref| <= 1e-10 for one-way inverse, one-way direct
+and the round trip.  Full TCo639 x 548 sizes are checked through
+size-independent properties (round trip, linearity, determinism)."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x), np.asarray(ref)
+    return float(np.max(np.max(np.abs(x - ref), axis=1) / np.maximum(np.max(np.abs(ref), axis=1), 1e-300)))
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _check(torch, T, nfld, grid="octahedral", seed=None):
+    from oracle.sht_oracle import SHTransformOracle, random_grid, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    o = SHTransformOracle(T, grid=grid, nfld=nfld)
+    sh = SHTransform(T, grid=grid, nfld=nfld)
+    assert sh.nspec_local == o.nspec and sh.npts_local == o.npts
+    a = random_spectral(T, nfld, seed=seed)
+    g = random_grid(T, nfld, o.npts, seed=None if seed is None else seed + 1)
+    da, dg = torch.from_numpy(a).cuda(), torch.from_numpy(g).cuda()
+    e_inv = rel(sh.inv_trans(da).cpu().numpy(), o.inv_trans(a))
+    e_dir = rel(sh.dir_trans(dg).cpu().numpy(), o.dir_trans(g))
+    e_rt = rel(sh.dir_trans(sh.inv_trans(da)).cpu().numpy(), a)
+    assert e_inv <= TOL and e_dir <= TOL and e_rt <= TOL, (e_inv, e_dir, e_rt)
+    return e_inv, e_dir, e_rt
+
+
+@pytest.mark.parametrize("name,T,nfld", [("tco79_f4", 79, 4), ("tco15_f3", 15, 3)])
+def test_golden(torch, name, T, nfld):
+    from paper_1908_06097_b200 import SHTransform
+
+    d = np.load(GOLD / f"{name}.npz")
+    sh = SHTransform(T, nfld=nfld)
+    assert rel(sh.inv_trans(torch.from_numpy(d["spec"]).cuda()).cpu().numpy(), d["inv"]) <= TOL
+    assert rel(sh.dir_trans(torch.from_numpy(d["grid"]).cuda()).cpu().numpy(), d["dir"]) <= TOL
+
+
+@pytest.mark.parametrize("T,nfld", [(1, 1), (2, 3), (7, 2), (79, 10), (79, 7), (95, 65), (159, 9), (319, 5)])
+def test_parity_small(torch, T, nfld):
+    _check(torch, T, nfld)
+
+
+def test_parity_tco639(torch):
+    # the paper's test case, a bounded field count the oracle finishes in seconds
+    _check(torch, 639, 6)
+
+
+def test_parity_regular_gaussian_grid(torch):
+    T = 47
+    _check(torch, T, 4, grid=np.full(2 * (T + 1), 2 * T + 2))
+
+
+def _next_prime(n):
+    def isp(k):
+        return k > 1 and all(k % d for d in range(2, int(k ** 0.5) + 1))
+    while not isp(n):
+        n += 1
+    return n
+
+
+def test_parity_reduced_grid_prime_rings(torch):
+    # non-octahedral reduced grid whose ring lengths are primes (Bluestein on every ring)
+    T = 40
+    north = []
+    for i in range(T + 1):
+        n = _next_prime(max(2 * i + 23, north[-1] + 1 if north else 0))
+        north.append(n)
+    nloen = np.array(north + north[::-1])
+    _check(torch, T, 3, grid=nloen)
+
+
+def test_roundtrip_full_size(torch):
+    """TCo639 x 548 fields (the bench workload): dir(inv(a)) = a to 1e-10."""
+    from oracle.sht_oracle import random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 639, 548
+    sh = SHTransform(T, nfld=nf)
+    a = torch.from_numpy(random_spectral(T, nf)).cuda()
+    b = sh.dir_trans(sh.inv_trans(a))
+    err = ((b - a).abs().amax(dim=1) / a.abs().amax(dim=1)).max().item()
+    assert err <= TOL, err
+
+
+def test_linearity_and_determinism(torch):
+    from oracle.sht_oracle import random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 319, 70
+    sh = SHTransform(T, nfld=nf)
+    a = torch.from_numpy(random_spectral(T, nf, seed=3)).cuda()
+    b = torch.from_numpy(random_spectral(T, nf, seed=4)).cuda()
+    ga, gb = sh.inv_trans(a), sh.inv_trans(b)
+    gab = sh.inv_trans(2.0 * a - b)
+    assert ((gab - (2.0 * ga - gb)).abs().max() / gab.abs().max()).item() <= 1e-13
+    # bitwise reproducible: no atomics in any reduction
+    assert torch.equal(sh.inv_trans(a), ga)
+    s1, s2 = sh.dir_trans(ga), sh.dir_trans(ga)
+    assert torch.equal(s1, s2)
+
+
+def test_host_arrays_and_streams(torch):
+    from oracle.sht_oracle import SHTransformOracle, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 63, 5
+    o = SHTransformOracle(T, nfld=nf)
+    sh = SHTransform(T, nfld=nf)
+    a = random_spectral(T, nf)
+    g = sh.inv_trans(a)                          # numpy in -> numpy out (e2e path)
+    assert isinstance(g, np.ndarray) and rel(g, o.inv_trans(a)) <= TOL
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        da = torch.from_numpy(a).cuda()
+        out = torch.empty(nf, sh.npts_local, dtype=torch.float64, device="cuda")
+        sh.inv_trans(da, out=out, stream=s)
+    s.synchronize()
+    assert rel(out.cpu().numpy(), o.inv_trans(a)) <= TOL
+
+
+def test_bad_inputs(torch):
+    from paper_1908_06097_b200 import ConfigurationError, SHTransform
+
+    sh = SHTransform(15, nfld=2)
+    with pytest.raises(ConfigurationError):
+        sh.inv_trans(torch.zeros(2, 10, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ConfigurationError):
+        sh.inv_trans(torch.zeros(2, sh.nspec_local, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ConfigurationError):
+        sh.inv_trans(torch.zeros(2, sh.nspec_local, dtype=torch.float64))
+    with pytest.raises(ConfigurationError):
+        SHTransform(0, nfld=1)
+    with pytest.raises(ConfigurationError):
+        SHTransform(10, nfld=0)
+    with pytest.raises(ConfigurationError):
+        SHTransform(10, grid="gaussian", nfld=1)
+
+
+def test_native_library_loaded(torch):
+    """The CUDA path is libsht.so from this tree (no silent fallback)."""
+    from paper_1908_06097_b200 import _lib
+
+    lib = _lib.load()
+    maps = Path("/proc/self/maps").read_text()
+    assert str(_lib.LIB_PATH) in maps
+    assert lib.sht_version() >= 100

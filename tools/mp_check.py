@@ -1,0 +1,55 @@
+"""Multi-rank parity check (run under torchrun): each rank's local slice of
+inv_trans / dir_trans / round trip vs the 1-rank CPU oracle.
+usage: torchrun --nproc-per-node N tools/mp_check.py T nfld [T nfld ...]"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle.sht_oracle import SHTransformOracle, random_grid, random_spectral  # noqa: E402
+from oracle.transposition import Layout  # noqa: E402
+from paper_1908_06097_b200 import SHTransform  # noqa: E402
+
+
+def rel(x, ref):
+    return float(np.max(np.max(np.abs(x - ref), axis=1) / np.max(np.abs(ref), axis=1)))
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    args = [int(x) for x in sys.argv[1:]]
+    worst = 0.0
+    for T, nf in zip(args[0::2], args[1::2]):
+        o = SHTransformOracle(T, nfld=nf)
+        lay = Layout(o, world)
+        sh = SHTransform(T, nfld=nf, group=dist.group.WORLD)
+        assert list(sh.m_list) == list(lay.M[rank]), "m partition differs from the restatement"
+        assert list(sh.ring_list) == lay.local_rings(rank), "ring partition differs"
+        a = random_spectral(T, nf)
+        g = random_grid(T, nf, o.npts)
+        la = torch.from_numpy(np.ascontiguousarray(lay.local_spec(a, rank))).cuda()
+        lg = torch.from_numpy(np.ascontiguousarray(lay.local_grid(g, rank))).cuda()
+        gi = sh.inv_trans(la).cpu().numpy()
+        sd = sh.dir_trans(lg).cpu().numpy()
+        rt = sh.dir_trans(sh.inv_trans(la)).cpu().numpy()
+        e = (rel(gi, lay.local_grid(o.inv_trans(a), rank)), rel(sd, lay.local_spec(o.dir_trans(g), rank)),
+             rel(rt, lay.local_spec(a, rank)))
+        print(f"rank {rank}/{world} T={T} nfld={nf}: inv {e[0]:.2e} dir {e[1]:.2e} rt {e[2]:.2e}", flush=True)
+        worst = max(worst, *e)
+        sh.close()
+    t = torch.tensor([worst], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print("MP_OK" if t.item() <= 1e-10 else f"MP_FAIL {t.item()}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if t.item() <= 1e-10 else 1)
+
+
+if __name__ == "__main__":
+    main()
