@@ -64,25 +64,35 @@ size_t leg_inv_smem();
 size_t leg_dir_smem();
 
 // ---------------------------------------------------------------- ring FFTs
-constexpr int kFftThreads = 512;
-constexpr int kFftMaxLen = 8192;                   // longest transform one CTA handles (smem bound)
-constexpr int kMaxStages = 24;
+constexpr int kMaxPasses = 8;
+constexpr int kFftMaxLen = 6912;   // longest transform one CTA handles (ping-pong buffers in smem)
+
+struct FftPass {       // one Stockham pass of a ring plan
+  int32_t radix;
+  int32_t ns;          // span: product of the radices already applied
+  int32_t nbf;         // butterflies per sequence = L / radix
+  int32_t pad;
+  uint64_t mag_nbf;    // multiply-shift (>> 40) divisors for nbf and ns
+  uint64_t mag_ns;
+  int64_t tw_off;      // twiddles W[k][r-1] = exp(-2 pi i r k / (ns radix)) in the arena
+};
 
 struct FftRing {       // one northern ring (and its southern mirror) on this rank
   int32_t n;           // points on the ring
   int32_t L;           // transform length (n, or the Bluestein length)
   int32_t mcap;        // M_i
-  int32_t nstage;
-  int8_t radix[kMaxStages];
-  int64_t tw_off;      // complex offset of W_L[k] = exp(-2 pi i k / L)
+  int32_t npass;
+  int32_t pass0;       // first pass in FftParams::passes
+  int32_t fp;          // field pairs per CTA
+  int32_t nb;          // sequences per FFT batch
+  int32_t pad;
+  uint64_t mag_L, mag_N, mag_M1;  // multiply-shift (>> 40) divisors for L, n, mcap + 1
   int64_t chirp_off;   // Bluestein chirp w_n = exp(-pi i n^2 / N), n < N   (-1: none)
   int64_t bhat_off;    // Bluestein kernel spectrum / L                     (-1: none)
   int64_t goff_n;      // offset of the northern ring in the local grid field
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
   double w;            // Gaussian weight
-  int32_t fp;          // field pairs per CTA
-  int32_t nb;          // sequences per pass
 };
 
 struct FftWork {       // one CTA of a ring-FFT launch
@@ -94,21 +104,23 @@ struct FftParams {
   int nfld;
   int64_t grid_ld;           // doubles per local grid field
   const FftRing* rings;
+  const FftPass* passes;
   const FftWork* work;
-  int nwork;
   const double2* tw;         // twiddle / chirp arena
   const int32_t* yrow;       // Fourier row of (ring, m)
 };
 
-// Launch the CTAs work[w0 .. w0+nw) of a ring-FFT pass with `smem` bytes of dynamic shared memory.
-void launch_fft_g2f(const FftParams& p, int w0, int nw, const double* grid, double* four, size_t smem,
-                    cudaStream_t s);
-void launch_fft_f2g(const FftParams& p, int w0, int nw, const double* four, double* grid, size_t smem,
-                    cudaStream_t s);
-// Complex values one pass can keep in flight for a plan with these radices.
-int fft_capacity(const std::vector<int>& radices);
-// Plan for a ring of n points: mixed radix {2,3,4,5,7,8,11,13} when n factors
-// over those, else Bluestein with the smallest 7-smooth L >= 2n-1 that fits.
+// Launch CTAs work[w0 .. w0+nw) of a ring-FFT class.  variant 0: radix <= 16,
+// 256 threads, 2 CTAs/SM; 1: radix <= 16, 512 threads; 2: prime radices up to
+// 31, 256 threads.  g2f: grid -> Fourier (in = grid), else Fourier -> grid.
+void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
+                size_t smem, cudaStream_t s);
+// Complex values one in-place pass of `variant` can hold for these radices.
+int fft_capacity(int variant, const std::vector<int>& radices);
+// Plan for a ring of n points: mixed radix (composite <= 16, primes <= 31)
+// when n factors over those, else Bluestein with a 13-smooth L >= 2n-1.
 int fft_choose(int n, std::vector<int>& radices, int& L, bool& bluestein);
+bool fft_needs_big(const std::vector<int>& radices);
+void fft_passes(int L, const std::vector<int>& radices, std::vector<FftPass>& out, std::vector<double2>& arena);
 
 }  // namespace sht

@@ -188,8 +188,9 @@ struct sht_plan {
   double* Y = nullptr;
   sht::FftRing* d_rings = nullptr;
   sht::FftWork* d_work = nullptr;
-  int nwork_small = 0, nwork_large = 0;
-  size_t smem_small = 0, smem_large = 0;
+  int fft_w0[3] = {0, 0, 0}, fft_nw[3] = {0, 0, 0};  // per ring-FFT kernel variant
+  size_t fft_smem[3] = {0, 0, 0};
+  sht::FftPass* d_passes = nullptr;
   double2* d_tw = nullptr;
   int32_t* d_yrow = nullptr;
   ncclComm_t comm = nullptr;
@@ -207,7 +208,7 @@ namespace sht {
 static void free_plan(sht_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
-                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X,
+                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_passes,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -341,7 +342,7 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   const int nlr = (int)p->my_rings.size();
   std::vector<FftRing> rings(nlr);
   std::vector<double2> arena;
-  std::map<int, int64_t> tw_of_L, chirp_of_N, bhat_of_N;
+  std::map<int, int64_t> chirp_of_N, bhat_of_N;
   std::vector<int32_t> yrow;
   int64_t go = 0;
   for (int lr = 0; lr < nlr; ++lr) {
@@ -354,8 +355,9 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   }
   p->grid_ld = go;
   const int npairs = (nfld + 1) / 2;
-  const size_t budget_small = 100 * 1024, budget_large = 220 * 1024;
-  std::vector<std::pair<int64_t, FftWork>> wsmall, wlarge;
+  const size_t budget_small = 108 * 1024, budget_large = 220 * 1024;
+  std::vector<std::pair<int64_t, FftWork>> wcls[3];  // per kernel variant
+  std::vector<FftPass> passes;
   int64_t nfour_local = 0;
   for (int lr = 0; lr < nlr; ++lr) {
     const int i = p->my_rings[lr];
@@ -370,18 +372,13 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     if (fft_choose(R.n, rad, L, blue))
       return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
     R.L = L;
-    R.nstage = (int)rad.size();
-    for (int s = 0; s < kMaxStages; ++s) R.radix[s] = s < R.nstage ? (int8_t)rad[s] : 0;
-    const long double two_pi = 6.283185307179586476925286766559005768L;
+    R.mag_L = ((uint64_t)1 << 40) / (uint64_t)L + 1;
+    R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
+    R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
+    R.npass = (int)rad.size();
+    R.pass0 = (int)passes.size();
+    fft_passes(L, rad, passes, arena);
     const long double pi_ld = 3.14159265358979323846264338327950288L;
-    if (!tw_of_L.count(L)) {
-      tw_of_L[L] = (int64_t)arena.size();
-      for (int k = 0; k < L; ++k) {
-        const long double a = -two_pi * (long double)k / (long double)L;
-        arena.push_back(make_double2((double)cosl(a), (double)sinl(a)));
-      }
-    }
-    R.tw_off = tw_of_L[L];
     R.chirp_off = R.bhat_off = -1;
     if (blue) {
       const int N = R.n;
@@ -414,42 +411,52 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
       const int s = p->m_owner[m];
       yrow.push_back((int32_t)(ybase[s][i] + p->lm_of_m[m]));
     }
-    // field pairs per CTA / sequences per pass: ping + pong buffers of nb
-    // sequences, plus the (M+1) x 2fp staging area of both hemispheres
+    // kernel variant, field pairs per CTA (fp) and sequences per FFT batch (nb):
+    // ping + pong buffers of nb sequences + a staging area of (M+1) rows x 2fp
+    // fields x {S, A}; prefer one batch (nb = 2 fp) and as many fields as fit.
     auto smem = [&](int fp, int nb) { return (2 * (size_t)nb * L + 4 * (size_t)(R.mcap + 1) * fp) * sizeof(double2); };
-    auto pick = [&](size_t budget, int& fpo, int& nbo) {
+    auto pick = [&](int variant, size_t budget, int& fpo, int& nbo) {
+      const int nbmax = fft_capacity(variant, rad) / L;
+      if (nbmax < 1) return false;
       for (int fp = std::min(npairs, 64); fp >= 1; --fp) {
-        if (smem(fp, 2 * fp) <= budget) {
+        const int nb = std::min(nbmax, 2 * fp);
+        if (nb == 2 * fp && smem(fp, nb) <= budget) {
           fpo = fp;
-          nbo = 2 * fp;
+          nbo = nb;
           return true;
         }
       }
-      if (smem(1, 1) <= budget) {
+      if (smem(1, 1) <= budget) {  // one sequence at a time (north, then south)
         fpo = 1;
         nbo = 1;
         return true;
       }
       return false;
     };
-    int fp = 0, nb = 0;
-    bool small = pick(budget_small, fp, nb);
-    if (!small && !pick(budget_large, fp, nb))
-      return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+    int fp = 0, nb = 0, variant = 0;
+    if (fft_needs_big(rad)) {
+      variant = 2;
+      if (!pick(2, budget_large, fp, nb))
+        return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
+    } else if (!pick(0, budget_small, fp, nb)) {
+      variant = 1;
+      if (!pick(1, budget_large, fp, nb))
+        return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
+    }
     R.fp = fp;
     R.nb = nb;
-    (small ? p->smem_small : p->smem_large) =
-        std::max(small ? p->smem_small : p->smem_large, smem(fp, nb));
-    for (int fp0 = 0; fp0 < npairs; fp0 += fp) (small ? wsmall : wlarge).push_back({(int64_t)L * R.nstage, {lr, fp0}});
+    p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(fp, nb));
+    const int64_t cost = (int64_t)2 * fp * L * R.npass * (blue ? 2 : 1);
+    for (int fp0 = 0; fp0 < npairs; fp0 += fp) wcls[variant].push_back({cost, {lr, fp0}});
   }
   auto bycost = [](const std::pair<int64_t, FftWork>& a, const std::pair<int64_t, FftWork>& b) { return a.first > b.first; };
-  std::stable_sort(wsmall.begin(), wsmall.end(), bycost);
-  std::stable_sort(wlarge.begin(), wlarge.end(), bycost);
   std::vector<FftWork> work;
-  for (auto& x : wlarge) work.push_back(x.second);
-  for (auto& x : wsmall) work.push_back(x.second);
-  p->nwork_large = (int)wlarge.size();
-  p->nwork_small = (int)wsmall.size();
+  for (int c : {1, 2, 0}) {  // 1-CTA/SM variants first, they carry the largest rings
+    std::stable_sort(wcls[c].begin(), wcls[c].end(), bycost);
+    p->fft_w0[c] = (int)work.size();
+    p->fft_nw[c] = (int)wcls[c].size();
+    for (auto& x : wcls[c]) work.push_back(x.second);
+  }
   int64_t npts_local = go;
   p->work_fft = 2.0 * nfld * (8.0 * (double)npts_local + 16.0 * (double)nfour_local);
   int64_t sent = 0;
@@ -473,6 +480,7 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   if (int rc = upload(&p->d_tiles_dir, td)) return rc;
   if (int rc = upload(&p->d_rings, rings)) return rc;
   if (int rc = upload(&p->d_work, work)) return rc;
+  if (int rc = upload(&p->d_passes, passes)) return rc;
   if (int rc = upload(&p->d_tw, arena)) return rc;
   if (int rc = upload(&p->d_yrow, yrow)) return rc;
   SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
@@ -542,8 +550,8 @@ static FftParams fft_params(const sht_plan* p) {
   fp.nfld = p->nfld;
   fp.grid_ld = p->grid_ld;
   fp.rings = p->d_rings;
+  fp.passes = p->d_passes;
   fp.work = p->d_work;
-  fp.nwork = p->nwork_large + p->nwork_small;
   fp.tw = p->d_tw;
   fp.yrow = p->d_yrow;
   return fp;
@@ -726,8 +734,7 @@ int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
     if (int rc = alltoall(p, true, s)) return rc;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][2], s));
   const FftParams fp = fft_params(p);
-  launch_fft_f2g(fp, 0, p->nwork_large, p->Y, grid, p->smem_large, s);
-  launch_fft_f2g(fp, p->nwork_large, p->nwork_small, p->Y, grid, p->smem_small, s);
+  for (int c : {1, 2, 0}) launch_fft(false, c, fp, p->fft_w0[c], p->fft_nw[c], p->Y, grid, p->fft_smem[c], s);
   SHT_CUDA_TRY(cudaGetLastError());
   if (prof) {
     SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][3], s));
@@ -744,8 +751,7 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][4], s));
   const FftParams fp = fft_params(p);
-  launch_fft_g2f(fp, 0, p->nwork_large, grid, p->Y, p->smem_large, s);
-  launch_fft_g2f(fp, p->nwork_large, p->nwork_small, grid, p->Y, p->smem_small, s);
+  for (int c : {1, 2, 0}) launch_fft(true, c, fp, p->fft_w0[c], p->fft_nw[c], grid, p->Y, p->fft_smem[c], s);
   SHT_CUDA_TRY(cudaGetLastError());
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][5], s));
   if (p->nranks > 1)
@@ -768,7 +774,8 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
 
 int sht_kernel_launches(const sht_plan* p, int* per_pair) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
-  const int fft = (p->nwork_large > 0) + (p->nwork_small > 0);
+  int fft = 0;
+  for (int c = 0; c < 3; ++c) fft += p->fft_nw[c] > 0;
   if (per_pair) *per_pair = (p->ntiles_inv > 0) + (p->ntiles_dir > 0) + 2 * fft;
   return SHT_OK;
 }

@@ -109,11 +109,14 @@ def test_size_matrix_golden(lib):
 def test_fft_plans(lib):
     from paper_1908_06097_b200 import fft_plan_info
 
-    assert fft_plan_info(20) == {"radices": [4, 5], "length": 20, "bluestein": False}
-    big = fft_plan_info(2576)                      # 2576 = 2^4 * 7 * 23 -> Bluestein
-    assert big["bluestein"] and big["length"] >= 2 * 2576 - 1
+    p20 = fft_plan_info(20)
+    assert p20["length"] == 20 and not p20["bluestein"] and len(p20["radices"]) == 2
+    assert fft_plan_info(2560)["radices"] and len(fft_plan_info(2560)["radices"]) == 3    # 16 x 16 x 10
+    assert not fft_plan_info(2576)["bluestein"]    # 2576 = 2^4 * 7 * 23: direct radix-23 pass
+    big = fft_plan_info(2572)                      # 2572 = 4 * 643 -> Bluestein
+    assert big["bluestein"] and big["length"] >= 2 * 2572 - 1
     assert int(np.prod(big["radices"])) == big["length"]
-    for n in range(20, 2600, 4):
+    for n in range(20, 2600, 4):  # every TCo639 ring
         info = fft_plan_info(n)
         assert int(np.prod(info["radices"])) == info["length"]
         assert info["length"] == n or info["bluestein"]
