@@ -74,8 +74,12 @@ struct FftPass {       // one Stockham pass of a ring plan
   int32_t pad;
   uint64_t mag_nbf;    // multiply-shift (>> 40) divisors for nbf and ns
   uint64_t mag_ns;
-  int64_t tw_off;      // twiddles W[k][r-1] = exp(-2 pi i r k / (ns radix)) in the arena
+  int32_t tstride;     // L / (ns radix): base twiddle of butterfly k is W_L^(k tstride)
+  int32_t pad2;
 };
+
+constexpr int kTwLo = 64;                          // two-level twiddle table: W_L^e = hi[e / 64] lo[e % 64]
+constexpr int kTwHi = (6912 + kTwLo - 1) / kTwLo;  // entries of hi for the longest transform
 
 struct FftRing {       // one northern ring (and its southern mirror) on this rank
   int32_t n;           // points on the ring
@@ -92,6 +96,7 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   int64_t goff_n;      // offset of the northern ring in the local grid field
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
+  int64_t tw2_off;     // arena offset of lo[0..63] = W_L^e, then hi[h] = W_L^(64 h), h < ceil(L/64)
   double w;            // Gaussian weight
 };
 
@@ -108,6 +113,7 @@ struct FftParams {
   const FftWork* work;
   const double2* tw;         // twiddle / chirp arena
   const int32_t* yrow;       // Fourier row of (ring, m)
+  int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT passes
 };
 
 // Launch CTAs work[w0 .. w0+nw) of a ring-FFT class.  variant 0: radix <= 16,
@@ -120,7 +126,10 @@ int fft_capacity(int variant, const std::vector<int>& radices);
 // Plan for a ring of n points: mixed radix (composite <= 16, primes <= 31)
 // when n factors over those, else Bluestein with a 13-smooth L >= 2n-1.
 int fft_choose(int n, std::vector<int>& radices, int& L, bool& bluestein);
+// Same with composite radices capped at `cap` (16, or 8 for the 1024-thread variant).
+int fft_choose(int n, int cap, std::vector<int>& radices, int& L, bool& bluestein);
 bool fft_needs_big(const std::vector<int>& radices);
-void fft_passes(int L, const std::vector<int>& radices, std::vector<FftPass>& out, std::vector<double2>& arena);
+void fft_passes(int L, const std::vector<int>& radices, std::vector<FftPass>& out, std::vector<double2>& arena,
+                int64_t& tw2_off);
 
 }  // namespace sht

@@ -52,6 +52,15 @@ constexpr int kLegThreads = 256;
 // Tile: rings r0..r0+63 (northern index) x fields f0..f0+63 of wavenumber lm.
 // Warp w: rings 32*(w&1).. , fields 16*(w>>1)..  -> 4 ring groups x 2 field groups
 // x {S.re, S.im, A.re, A.im} DMMA accumulators (64 doubles per thread).
+// Persistent: the next tile's first pipeline stages are issued before the
+// current tile's epilogue stores, so tile switches do not drain the pipeline.
+struct InvTile {
+  int lm, r0, f0, K, nk;
+  const double* P;
+  const double* S;
+  int kp;
+};
+
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(16) double sm[];
@@ -60,43 +69,56 @@ __global__ void __launch_bounds__(kLegThreads, 1)
   const int wr = warp & 1, wf = warp >> 1;
   const int lr = lane >> 2, lc = lane & 3;
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-    __syncthreads();
-    const int t = s_tile;
-    if (t >= p.ntiles) break;
+  auto make = [&](int t) {
+    InvTile c;
     const LegTile tile = p.tiles[t];
-    const int lm = tile.lm, r0 = tile.r0, f0 = tile.f0;
-    const int m = p.lm_m[lm];
-    const int i0 = p.lm_i0[lm];
-    const int kp = p.lm_kp[lm];
-    const int K = p.T - m + 1;
-    const int nk = (K + kInvKc - 1) / kInvKc;
-    const double* P = p.ptab + p.lm_poff[lm] + (int64_t)(r0 - i0) * kp;
-    const double* S = spec + 2 * p.lm_soff[lm];
-
-    auto load_stage = [&](int kc, int st) {
-      double* Ps = sm + st * kInvStageDbl;
-      double* Ss = Ps + kInvPDbl;
+    c.lm = tile.lm;
+    c.r0 = tile.r0;
+    c.f0 = tile.f0;
+    const int m = p.lm_m[c.lm];
+    c.kp = p.lm_kp[c.lm];
+    c.K = p.T - m + 1;
+    c.nk = (c.K + kInvKc - 1) / kInvKc;
+    c.P = p.ptab + p.lm_poff[c.lm] + (int64_t)(c.r0 - p.lm_i0[c.lm]) * c.kp;
+    c.S = spec + 2 * p.lm_soff[c.lm];
+    return c;
+  };
+  auto load_stage = [&](const InvTile& c, int kc, int st) {
+    double* Ps = sm + st * kInvStageDbl;
+    double* Ss = Ps + kInvPDbl;
 #pragma unroll
-      for (int it = 0; it < (kInvRings * (kInvKc / 2)) / kLegThreads; ++it) {
-        const int c = tid + it * kLegThreads;
-        const int row = c >> 4, col = c & 15;
-        const bool v = (r0 + row) < p.nh;
-        const double* src = v ? P + (int64_t)row * kp + kc * kInvKc + col * 2 : p.ptab;
-        cp_async16(Ps + row * kInvPStr + col * 2, src, v);
-      }
+    for (int it = 0; it < (kInvRings * (kInvKc / 2)) / kLegThreads; ++it) {
+      const int q = tid + it * kLegThreads;
+      const int row = q >> 4, col = q & 15;
+      const bool v = (c.r0 + row) < p.nh;
+      const double* src = v ? c.P + (int64_t)row * c.kp + kc * kInvKc + col * 2 : p.ptab;
+      cp_async16(Ps + row * kInvPStr + col * 2, src, v);
+    }
 #pragma unroll
-      for (int it = 0; it < (kLegFields * kInvKc) / kLegThreads; ++it) {
-        const int c = tid + it * kLegThreads;
-        const int f = c >> 5, n = c & 31;
-        const int kk = kc * kInvKc + n;
-        const bool v = (f0 + f) < p.nfld && kk < K;
-        const double* src = v ? S + (int64_t)(f0 + f) * p.spec_ld + 2 * kk : spec;
-        cp_async16(Ss + f * kInvSStr + 2 * n, src, v);
-      }
-    };
+    for (int it = 0; it < (kLegFields * kInvKc) / kLegThreads; ++it) {
+      const int q = tid + it * kLegThreads;
+      const int f = q >> 5, n = q & 31;
+      const int kk = kc * kInvKc + n;
+      const bool v = (c.f0 + f) < p.nfld && kk < c.K;
+      const double* src = v ? c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kk : spec;
+      cp_async16(Ss + f * kInvSStr + 2 * n, src, v);
+    }
+  };
+  auto prologue = [&](const InvTile& c) {
+#pragma unroll
+    for (int st = 0; st < kInvStages - 1; ++st) {
+      if (st < c.nk) load_stage(c, st, st);
+      cp_async_commit();
+    }
+  };
 
+  if (tid == 0) s_tile = atomicAdd(p.counter, 1);
+  __syncthreads();
+  int t = s_tile;
+  if (t >= p.ntiles) return;
+  InvTile c = make(t);
+  prologue(c);
+  while (true) {
     double acc[4][2][4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g)
@@ -104,20 +126,14 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
+    const bool active = (c.r0 + wr * 32 < p.nh) && (c.f0 + wf * 16 < p.nfld);
 
-    const bool active = (r0 + wr * 32 < p.nh) && (f0 + wf * 16 < p.nfld);
-
-#pragma unroll
-    for (int s = 0; s < kInvStages - 1; ++s) {
-      if (s < nk) load_stage(s, s);
-      cp_async_commit();
-    }
-    for (int kc = 0; kc < nk; ++kc) {
+    for (int kc = 0; kc < c.nk; ++kc) {
       cp_async_wait<kInvStages - 2>();
       __syncthreads();
       {
         const int nx = kc + kInvStages - 1;
-        if (nx < nk) load_stage(nx, nx % kInvStages);
+        if (nx < c.nk) load_stage(c, nx, nx % kInvStages);
         cp_async_commit();
       }
       if (active) {
@@ -146,21 +162,28 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         }
       }
     }
-    cp_async_wait<0>();
+    __syncthreads();  // every warp is done with the stage buffers
+    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
     __syncthreads();
+    const int tn = s_tile;
+    InvTile cn;
+    if (tn < p.ntiles) {
+      cn = make(tn);
+      prologue(cn);  // next tile's loads overlap this tile's stores
+    }
 
     if (active) {
       const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const int ring = r0 + wr * 32 + g * 8 + lr;
+        const int ring = c.r0 + wr * 32 + g * 8 + lr;
         if (ring < p.nh) {
-          double* dst = four + (int64_t)(p.xbase[ring] + lm) * rowd;
+          double* dst = four + (int64_t)(p.xbase[ring] + c.lm) * rowd;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int f = f0 + wf * 16 + h * 8 + 2 * lc + e;
+              const int f = c.f0 + wf * 16 + h * 8 + 2 * lc + e;
               if (f < p.nfld) {
                 double2* d = reinterpret_cast<double2*>(dst + (int64_t)f * 4);
                 d[0] = make_double2(acc[g][h][0][e], acc[g][h][1][e]);
@@ -170,7 +193,10 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         }
       }
     }
+    if (tn >= p.ntiles) break;
+    c = cn;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ leg_dir
@@ -183,6 +209,11 @@ constexpr int kDirStageDbl = kDirPDbl + 2 * kDirBDbl;
 
 // Tile: n-m offsets n0..n0+127 (64 even-parity rows, 64 odd) x fields f0..f0+63.
 // Warp w: n 64*(w&1).. (4 groups of 8 (S,A) row pairs), fields 16*(w>>1)..
+struct DirTile {
+  int lm, n0, f0, K, i0, nrings, nk, kp;
+  const double* P;
+};
+
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_dir_kernel(const LegParams p, const double* __restrict__ four, double* __restrict__ spec) {
   extern __shared__ __align__(16) double sm[];
@@ -192,47 +223,62 @@ __global__ void __launch_bounds__(kLegThreads, 1)
   const int lr = lane >> 2, lc = lane & 3;
   const int64_t rowd = (int64_t)p.nfld * 4;
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-    __syncthreads();
-    const int t = s_tile;
-    if (t >= p.ntiles) break;
+  auto make = [&](int t) {
+    DirTile c;
     const LegTile tile = p.tiles[t];
-    const int lm = tile.lm, n0 = tile.r0, f0 = tile.f0;
-    const int m = p.lm_m[lm];
-    const int i0 = p.lm_i0[lm];
-    const int kp = p.lm_kp[lm];
-    const int K = p.T - m + 1;
-    const int nrings = p.nh - i0;
-    const int nk = (nrings + kDirKc - 1) / kDirKc;
-    const double* P = p.ptab + p.lm_poff[lm];
-
-    auto load_stage = [&](int kc, int st) {
-      double* Ps = sm + st * kDirStageDbl;
-      double* Ss = Ps + kDirPDbl;
-      double* As = Ss + kDirBDbl;
+    c.lm = tile.lm;
+    c.n0 = tile.r0;
+    c.f0 = tile.f0;
+    const int m = p.lm_m[c.lm];
+    c.i0 = p.lm_i0[c.lm];
+    c.kp = p.lm_kp[c.lm];
+    c.K = p.T - m + 1;
+    c.nrings = p.nh - c.i0;
+    c.nk = (c.nrings + kDirKc - 1) / kDirKc;
+    c.P = p.ptab + p.lm_poff[c.lm];
+    return c;
+  };
+  auto load_stage = [&](const DirTile& c, int kc, int st) {
+    double* Ps = sm + st * kDirStageDbl;
+    double* Ss = Ps + kDirPDbl;
+    double* As = Ss + kDirBDbl;
 #pragma unroll
-      for (int it = 0; it < (kDirKc * (kDirN / 2)) / kLegThreads; ++it) {
-        const int c = tid + it * kLegThreads;
-        const int rr = c >> 6, cc = c & 63;
-        const int ring = kc * kDirKc + rr;  // relative to i0
-        const int nn = n0 + 2 * cc;
-        const bool v = ring < nrings && nn < K;
-        const double* src = v ? P + (int64_t)ring * kp + nn : p.ptab;
-        cp_async16(Ps + rr * kDirPStr + 2 * cc, src, v);
-      }
+    for (int it = 0; it < (kDirKc * (kDirN / 2)) / kLegThreads; ++it) {
+      const int q = tid + it * kLegThreads;
+      const int rr = q >> 6, cc = q & 63;
+      const int ring = kc * kDirKc + rr;  // relative to i0
+      const int nn = c.n0 + 2 * cc;
+      const bool v = ring < c.nrings && nn < c.K;
+      const double* src = v ? c.P + (int64_t)ring * c.kp + nn : p.ptab;
+      cp_async16(Ps + rr * kDirPStr + 2 * cc, src, v);
+    }
 #pragma unroll
-      for (int it = 0; it < (kDirKc * kLegFields * 2) / kLegThreads; ++it) {
-        const int c = tid + it * kLegThreads;
-        const int rr = c >> 7, rem = c & 127;
-        const int f = rem >> 1, half = rem & 1;
-        const int ring = kc * kDirKc + rr;
-        const bool v = ring < nrings && (f0 + f) < p.nfld;
-        const double* src = v ? four + (int64_t)(p.xbase[i0 + ring] + lm) * rowd + (int64_t)(f0 + f) * 4 + 2 * half : four;
-        cp_async16((half ? As : Ss) + rr * kDirBStr + 2 * f, src, v);
-      }
-    };
+    for (int it = 0; it < (kDirKc * kLegFields * 2) / kLegThreads; ++it) {
+      const int q = tid + it * kLegThreads;
+      const int rr = q >> 7, rem = q & 127;
+      const int f = rem >> 1, half = rem & 1;
+      const int ring = kc * kDirKc + rr;
+      const bool v = ring < c.nrings && (c.f0 + f) < p.nfld;
+      const double* src =
+          v ? four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd + (int64_t)(c.f0 + f) * 4 + 2 * half : four;
+      cp_async16((half ? As : Ss) + rr * kDirBStr + 2 * f, src, v);
+    }
+  };
+  auto prologue = [&](const DirTile& c) {
+#pragma unroll
+    for (int st = 0; st < kDirStages - 1; ++st) {
+      if (st < c.nk) load_stage(c, st, st);
+      cp_async_commit();
+    }
+  };
 
+  if (tid == 0) s_tile = atomicAdd(p.counter, 1);
+  __syncthreads();
+  int t = s_tile;
+  if (t >= p.ntiles) return;
+  DirTile c = make(t);
+  prologue(c);
+  while (true) {
     double acc[4][2][4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g)
@@ -240,20 +286,14 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
+    const bool active = (c.n0 + wn * 64 < c.K) && (c.f0 + wf * 16 < p.nfld);
 
-    const bool active = (n0 + wn * 64 < K) && (f0 + wf * 16 < p.nfld);
-
-#pragma unroll
-    for (int s = 0; s < kDirStages - 1; ++s) {
-      if (s < nk) load_stage(s, s);
-      cp_async_commit();
-    }
-    for (int kc = 0; kc < nk; ++kc) {
+    for (int kc = 0; kc < c.nk; ++kc) {
       cp_async_wait<kDirStages - 2>();
       __syncthreads();
       {
         const int nx = kc + kDirStages - 1;
-        if (nx < nk) load_stage(nx, nx % kDirStages);
+        if (nx < c.nk) load_stage(c, nx, nx % kDirStages);
         cp_async_commit();
       }
       if (active) {
@@ -283,30 +323,40 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         }
       }
     }
-    cp_async_wait<0>();
     __syncthreads();
+    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int tn = s_tile;
+    DirTile cn;
+    if (tn < p.ntiles) {
+      cn = make(tn);
+      prologue(cn);
+    }
 
     if (active) {
-      const int64_t soff = 2 * p.lm_soff[lm];
+      const int64_t soff = 2 * p.lm_soff[c.lm];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const int ns = n0 + wn * 64 + 2 * (g * 8 + lr);
-        if (ns < K) {
+        const int ns = c.n0 + wn * 64 + 2 * (g * 8 + lr);
+        if (ns < c.K) {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int f = f0 + wf * 16 + h * 8 + 2 * lc + e;
+              const int f = c.f0 + wf * 16 + h * 8 + 2 * lc + e;
               if (f < p.nfld) {
                 double2* d = reinterpret_cast<double2*>(spec + (int64_t)f * p.spec_ld + soff + 2 * ns);
                 d[0] = make_double2(acc[g][h][0][e], acc[g][h][1][e]);
-                if (ns + 1 < K) d[1] = make_double2(acc[g][h][2][e], acc[g][h][3][e]);
+                if (ns + 1 < c.K) d[1] = make_double2(acc[g][h][2][e], acc[g][h][3][e]);
               }
             }
         }
       }
     }
+    if (tn >= p.ntiles) break;
+    c = cn;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ leg_poly

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -201,6 +202,7 @@ struct sht_plan {
   bool hist_inv[kHist] = {};               // set k holds the events of an inverse transform
   int hist_cur = 0, hist_done = 0;
   float setup_ms = 0.f;
+  int fft_debug = 0;
 };
 
 namespace sht {
@@ -320,21 +322,18 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   p->ptab_len = po;
   p->work_leg = 2.0 * leg_flops;
 
-  // Legendre tiles (largest K first: the persistent scheduler then behaves like LPT)
+  // Legendre tiles, wavenumber-major with m ascending (K = T-m+1 descending):
+  // the persistent tile queue then runs the largest GEMMs first (LPT) and the
+  // ~150 tiles in flight touch only 2-4 wavenumbers, whose P-table rows and
+  // spectral / Fourier blocks stay resident in L2 across ring / n / field tiles.
   std::vector<LegTile> ti, td;
   for (int lm = 0; lm < nlm; ++lm) {
     const int K = T - p->my_m[lm] + 1;
     for (int r0 = lm_i0[lm]; r0 < nh; r0 += kInvRings)
       for (int f0 = 0; f0 < nfld; f0 += kLegFields) ti.push_back({lm, r0, f0, 0});
-    for (int n0 = 0; n0 < K; n0 += kDirN)
-      for (int f0 = 0; f0 < nfld; f0 += kLegFields) td.push_back({lm, n0, f0, 0});
+    for (int f0 = 0; f0 < nfld; f0 += kLegFields)
+      for (int n0 = 0; n0 < K; n0 += kDirN) td.push_back({lm, n0, f0, 0});
   }
-  auto kof = [&](const LegTile& t) { return T - p->my_m[t.lm] + 1; };
-  std::stable_sort(ti.begin(), ti.end(), [&](const LegTile& a, const LegTile& b) { return kof(a) > kof(b); });
-  auto dwork = [&](const LegTile& t) {
-    return (int64_t)(nh - lm_i0[t.lm]) * std::min(kDirN, kof(t) - t.r0);
-  };
-  std::stable_sort(td.begin(), td.end(), [&](const LegTile& a, const LegTile& b) { return dwork(a) > dwork(b); });
   p->ntiles_inv = (int)ti.size();
   p->ntiles_dir = (int)td.size();
 
@@ -369,15 +368,26 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     std::vector<int> rad;
     int L = 0;
     bool blue = false;
-    if (fft_choose(R.n, rad, L, blue))
+    if (fft_choose(R.n, 16, rad, L, blue))
       return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
+    // variant: 2 if a prime radix > 16 is needed; 0 if a 256-thread CTA fits in
+    // ~108 KB (2 CTAs/SM); else 1 (1024 threads, radices <= 8)
+    int variant = fft_needs_big(rad) ? 2 : 0;
+    if (variant == 0) {
+      const size_t one = (2 * (size_t)std::min(2, 2 * npairs) * L + 4 * (size_t)(g.mcap[i] + 1)) * sizeof(double2);
+      if (one > budget_small) {
+        variant = 1;
+        if (fft_choose(R.n, 8, rad, L, blue))
+          return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
+      }
+    }
     R.L = L;
     R.mag_L = ((uint64_t)1 << 40) / (uint64_t)L + 1;
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
     R.npass = (int)rad.size();
     R.pass0 = (int)passes.size();
-    fft_passes(L, rad, passes, arena);
+    fft_passes(L, rad, passes, arena, R.tw2_off);
     const long double pi_ld = 3.14159265358979323846264338327950288L;
     R.chirp_off = R.bhat_off = -1;
     if (blue) {
@@ -433,16 +443,9 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
       }
       return false;
     };
-    int fp = 0, nb = 0, variant = 0;
-    if (fft_needs_big(rad)) {
-      variant = 2;
-      if (!pick(2, budget_large, fp, nb))
-        return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
-    } else if (!pick(0, budget_small, fp, nb)) {
-      variant = 1;
-      if (!pick(1, budget_large, fp, nb))
-        return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
-    }
+    int fp = 0, nb = 0;
+    if (!pick(variant, variant == 0 ? budget_small : budget_large, fp, nb))
+      return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
     R.fp = fp;
     R.nb = nb;
     p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(fp, nb));
@@ -554,6 +557,7 @@ static FftParams fft_params(const sht_plan* p) {
   fp.work = p->d_work;
   fp.tw = p->d_tw;
   fp.yrow = p->d_yrow;
+  fp.debug = p->fft_debug;
   return fp;
 }
 
@@ -678,6 +682,7 @@ int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, in
   p->rank = rank;
   p->nranks = nranks;
   p->flags = flags;
+  if (const char* dbg = getenv("SHT_FFT_DEBUG")) p->fft_debug = atoi(dbg);
   int rc = make_geometry(truncation, ndgl, nloen, p->g);
   if (!rc) rc = build_plan(p, nccl_unique_id);
   if (rc) {
