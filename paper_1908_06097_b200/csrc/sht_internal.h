@@ -23,14 +23,14 @@ int fail(int code, const std::string& msg);
   } while (0)
 
 // ---------------------------------------------------------------- Legendre GEMM tiling
-// leg_inv: CTA tile = 64 northern rings x 64 fields, k-chunk = 32 wavenumbers n.
-// leg_dir: CTA tile = 128 wavenumbers n x 64 fields, k-chunk = 16 rings.
+// leg_inv: CTA tile = 64 northern rings x 64 fields, k-chunk = 64 wavenumbers n.
+// leg_dir: CTA tile = 128 wavenumbers n x 64 fields, k-chunk = 32 rings.
 constexpr int kLegFields = 64;
 constexpr int kInvRings = 64;
-constexpr int kInvKc = 32;
+constexpr int kInvKc = 64;
 constexpr int kDirN = 128;
-constexpr int kDirKc = 16;
-constexpr int kPtabPad = 32;  // P-table rows are padded (with zeros) to a multiple of this
+constexpr int kDirKc = 32;
+constexpr int kPtabPad = 64;  // P-table rows are padded (with zeros) to a multiple of this
 
 struct LegTile {  // one output tile of a Legendre GEMM
   int32_t lm;     // local wavenumber index
@@ -53,6 +53,7 @@ struct LegParams {
   const LegTile* tiles;
   int ntiles;
   int* counter;              // persistent-scheduler ticket
+  int debug;                 // profiling only (SHT_LEG_DEBUG): bit 0 skips operand loads, bit 1 skips DMMA
 };
 
 void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s);

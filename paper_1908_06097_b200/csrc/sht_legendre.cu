@@ -41,9 +41,9 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ------------------------------------------------------------------ leg_inv
-constexpr int kInvStages = 3;
-constexpr int kInvPStr = kInvKc + 8;          // 40 doubles: rows of P tile (== 8 mod 16 -> no LDS.128 conflicts)
-constexpr int kInvSStr = 2 * kInvKc + 2;      // 66 doubles: field rows of the spectral tile (== 2 mod 16)
+constexpr int kInvStages = 2;
+constexpr int kInvPStr = kInvKc + 8;          // 72 doubles: rows of P tile (== 8 mod 16 -> no LDS.128 conflicts)
+constexpr int kInvSStr = 2 * kInvKc + 2;      // 130 doubles: field rows of the spectral tile (== 2 mod 16)
 constexpr int kInvPDbl = kInvRings * kInvPStr;
 constexpr int kInvSDbl = kLegFields * kInvSStr;
 constexpr int kInvStageDbl = kInvPDbl + kInvSDbl;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 #pragma unroll
     for (int it = 0; it < (kInvRings * (kInvKc / 2)) / kLegThreads; ++it) {
       const int q = tid + it * kLegThreads;
-      const int row = q >> 4, col = q & 15;
+      const int row = q / (kInvKc / 2), col = q % (kInvKc / 2);
       const bool v = (c.r0 + row) < p.nh;
       const double* src = v ? c.P + (int64_t)row * c.kp + kc * kInvKc + col * 2 : p.ptab;
       cp_async16(Ps + row * kInvPStr + col * 2, src, v);
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 #pragma unroll
     for (int it = 0; it < (kLegFields * kInvKc) / kLegThreads; ++it) {
       const int q = tid + it * kLegThreads;
-      const int f = q >> 5, n = q & 31;
+      const int f = q / kInvKc, n = q % kInvKc;
       const int kk = kc * kInvKc + n;
       const bool v = (c.f0 + f) < p.nfld && kk < c.K;
       const double* src = v ? c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kk : spec;
@@ -127,20 +127,25 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
     const bool active = (c.r0 + wr * 32 < p.nh) && (c.f0 + wf * 16 < p.nfld);
+    // warp-uniform trims of the ragged edges: 8-ring groups, 8-field groups, 8-n sub-steps
+    const int gmax = min(4, max(0, (p.nh - c.r0 - wr * 32 + 7) / 8));
+    const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
       cp_async_wait<kInvStages - 2>();
       __syncthreads();
       {
         const int nx = kc + kInvStages - 1;
-        if (nx < c.nk) load_stage(c, nx, nx % kInvStages);
+        if (nx < c.nk && !(p.debug & 1)) load_stage(c, nx, nx % kInvStages);
         cp_async_commit();
       }
-      if (active) {
+      if (active && !(p.debug & 2)) {
         const double* Ps = sm + (kc % kInvStages) * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
         const double* Ss = sm + (kc % kInvStages) * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
+        const int smax = min(kInvKc / 8, (c.K - kc * kInvKc + 7) / 8);
 #pragma unroll
         for (int sub = 0; sub < kInvKc / 8; ++sub) {
+          if (sub >= smax) break;
           double2 a[4], bs[2], ba[2];
 #pragma unroll
           for (int g = 0; g < 4; ++g) a[g] = *reinterpret_cast<const double2*>(Ps + g * 8 * kInvPStr + sub * 8);
@@ -154,10 +159,12 @@ __global__ void __launch_bounds__(kLegThreads, 1)
           for (int g = 0; g < 4; ++g)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
-              dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
-              dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
-              dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+              if (g < gmax && h < hmax) {
+                dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
+                dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
+                dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
+                dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+              }
             }
         }
       }
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       prologue(cn);  // next tile's loads overlap this tile's stores
     }
 
-    if (active) {
+    if (active && !(p.debug & 4)) {
       const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 }
 
 // ------------------------------------------------------------------ leg_dir
-constexpr int kDirStages = 3;
+constexpr int kDirStages = 2;
 constexpr int kDirPStr = kDirN + 4;            // 132: P tile [ring][n]          (== 4 mod 16)
 constexpr int kDirBStr = 2 * kLegFields + 4;   // 132: S / A tiles [ring][field][re,im]
 constexpr int kDirPDbl = kDirKc * kDirPStr;
@@ -287,21 +294,26 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
     const bool active = (c.n0 + wn * 64 < c.K) && (c.f0 + wf * 16 < p.nfld);
+    // warp-uniform trims: 16-n row-pair groups, 8-field groups, 4-ring k-steps
+    const int gmax = min(4, max(0, (c.K - c.n0 - wn * 64 + 15) / 16));
+    const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
       cp_async_wait<kDirStages - 2>();
       __syncthreads();
       {
         const int nx = kc + kDirStages - 1;
-        if (nx < c.nk) load_stage(c, nx, nx % kDirStages);
+        if (nx < c.nk && !(p.debug & 1)) load_stage(c, nx, nx % kDirStages);
         cp_async_commit();
       }
-      if (active) {
+      if (active && !(p.debug & 2)) {
         const double* Ps = sm + (kc % kDirStages) * kDirStageDbl + lc * kDirPStr + wn * 64 + 2 * lr;
         const double* Ss = sm + (kc % kDirStages) * kDirStageDbl + kDirPDbl + lc * kDirBStr + 2 * (wf * 16 + lr);
         const double* As = Ss + kDirBDbl;
+        const int kmax = min(kDirKc / 4, (c.nrings - kc * kDirKc + 3) / 4);
 #pragma unroll
         for (int ks = 0; ks < kDirKc / 4; ++ks) {
+          if (ks >= kmax) break;
           double2 a[4], bs[2], ba[2];
 #pragma unroll
           for (int g = 0; g < 4; ++g)
@@ -315,10 +327,12 @@ __global__ void __launch_bounds__(kLegThreads, 1)
           for (int g = 0; g < 4; ++g)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
-              dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
-              dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
-              dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+              if (g < gmax && h < hmax) {
+                dmma(acc[g][h][0][0], acc[g][h][0][1], a[g].x, bs[h].x);
+                dmma(acc[g][h][1][0], acc[g][h][1][1], a[g].x, bs[h].y);
+                dmma(acc[g][h][2][0], acc[g][h][2][1], a[g].y, ba[h].x);
+                dmma(acc[g][h][3][0], acc[g][h][3][1], a[g].y, ba[h].y);
+              }
             }
         }
       }
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       prologue(cn);
     }
 
-    if (active) {
+    if (active && !(p.debug & 4)) {
       const int64_t soff = 2 * p.lm_soff[c.lm];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {

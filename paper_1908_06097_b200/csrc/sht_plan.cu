@@ -203,6 +203,7 @@ struct sht_plan {
   int hist_cur = 0, hist_done = 0;
   float setup_ms = 0.f;
   int fft_debug = 0;
+  int leg_debug = 0;
 };
 
 namespace sht {
@@ -545,6 +546,7 @@ static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles,
   lp.tiles = tiles;
   lp.ntiles = ntiles;
   lp.counter = counter;
+  lp.debug = p->leg_debug;
   return lp;
 }
 
@@ -683,6 +685,7 @@ int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, in
   p->nranks = nranks;
   p->flags = flags;
   if (const char* dbg = getenv("SHT_FFT_DEBUG")) p->fft_debug = atoi(dbg);
+  if (const char* dbg = getenv("SHT_LEG_DEBUG")) p->leg_debug = atoi(dbg);
   int rc = make_geometry(truncation, ndgl, nloen, p->g);
   if (!rc) rc = build_plan(p, nccl_unique_id);
   if (rc) {
