@@ -2,19 +2,24 @@
 // K5 fft_f2g: Fourier -> grid) on the variable-length octahedral rings.
 //
 // One CTA owns one ring PAIR (northern ring i and its southern mirror, same
-// length N) for a group of field pairs.  Two real fields are packed into one
-// complex sequence (z = x_a + i x_b), so every transform is a complex DFT of
-// length N; the pair is separated with Z_m / conj(Z_{N-m}).
+// length N) for a range of field pairs, processed in batches.  Two real
+// fields are packed into one complex sequence (z = x_a + i x_b), so every
+// transform is a complex DFT of length N; the pair is separated with Z_m /
+// conj(Z_{N-m}).
 //
-// The DFT is a self-sorting Stockham FFT ping-ponging between two shared-
-// memory buffers, in as few passes as possible: each pass is one radix-R
-// butterfly per thread held entirely in registers, with R a composite radix
-// <= 16 or a prime <= 31 (straight-line codelets generated by
-// tools/gen_codelets.py), so a 2560-point ring takes 3 passes (16,16,10) and
-// a 2576-point ring 3 passes (23,7,16).  Per-pass twiddles are stored [k][r]
-// so a warp's twiddle loads are contiguous; butterfly indices come from
-// multiply-shift division (no integer divide).  Rings with a prime factor
-// > 31 use Bluestein's algorithm with a 13-smooth length L >= 2N-1.
+// The DFT is an in-place "pencil" FFT in shared memory: L = R_0 R_1 ... R_{d-1}
+// (d <= 4, R_j <= 16, or a prime <= 31); in step j every thread owns whole
+// pencils of R_j points (stride S_j), loads them, runs a straight-line
+// codelet (tools/gen_codelets.py) in registers, applies the step's twiddles
+// (base twiddle from a 2-level table in shared memory, powers by recurrence)
+// and writes them back to the same addresses.  No value crosses a barrier in
+// registers and no second buffer is needed, so a 2576-point ring pair for one
+// field pair needs 82 KB and two CTAs share an SM.  The decimation-in-time
+// order leaves the spectrum digit-reversed; the transposed algorithm (steps in
+// reverse order, twiddles before the codelet) maps digit-reversed input back
+// to natural order.  Rings with a prime factor > 31 use Bluestein's algorithm
+// with a 13-smooth L >= 2N-1: DIT FFT, product with the kernel spectrum
+// (stored digit-reversed, fused into the last step), reverse FFT.
 //
 // Fusions: g2f scales by 1/N and combines the two hemispheres into the
 // parity rows the Legendre GEMM consumes, S' = w_i (F_N + F_S) and
@@ -49,143 +54,168 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Kernel variants: V0 radix <= 16, 256 threads, 2 CTAs/SM; V1 radix <= 16,
-// 512 threads, 1 CTA/SM (long rings); V2 radix <= 31, 256 threads, 1 CTA/SM.
 template <int V>
 struct FftCfg {
-  static constexpr int kThreads = V == 1 ? 1024 : 256;
-  static constexpr int kMinBlocks = V == 0 ? 2 : 1;
-  static constexpr bool kBig = V == 2;
-  // radices compiled into the pass switch (V1 plans use composites <= 8 and lone primes <= 13)
+  static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = V == 1 ? 2 : 1;
   template <int R>
   static constexpr bool has() {
-    return V == 1 ? (R <= 8 || R == 11 || R == 13) : true;
+    return V == 1 ? (R <= 16) : true;
   }
 };
 
-// One Stockham pass (in -> out, ping-pong buffers) over nseq sequences of
-// length L.  Small radices take two butterflies per iteration so more
-// twiddle / shared loads are in flight.  kPost: the last pass of Bluestein's
-// first FFT -- the pointwise product with the kernel spectrum and the
-// conjugation are applied on the way out (out = conj(X * bhat)).
-template <int R, int V, bool kPost>
-__device__ __forceinline__ void pass_run(const double2* __restrict__ in, double2* __restrict__ out, int nseq, int L,
-                                         const FftPass& ps, const double2* __restrict__ W,
-                                         const double2* __restrict__ bhat) {
+// One pencil step over nseq sequences of length L (in place).  kFwd: DIT
+// step (codelet, then twiddle); else transposed step (twiddle, then codelet).
+// kPost: last DIT step of Bluestein's first FFT: store conj(X * bhat).
+template <int R, int V, bool kFwd, bool kPost>
+__device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, int L, const FftStep& st, bool tw,
+                                         const double2* __restrict__ tw2, const double2* __restrict__ bhat) {
   constexpr int NT = FftCfg<V>::kThreads;
-  constexpr int U = 1;
-  const int nbf = ps.nbf, Ns = ps.ns;
-  const int total = nseq * nbf;
-  for (int b0 = threadIdx.x; b0 < total; b0 += U * NT) {
-    double2 v[U][R];
-    int ob[U], kk[U];
+  const int np = st.np, S = st.S;
+  const int total = nseq * np;
+  for (int b = threadIdx.x; b < total; b += NT) {
+    const int q = fdiv(b, st.mag_np);
+    const int pp = b - q * np;
+    const int blk = fdiv(pp, st.mag_S);
+    const int s = pp - blk * S;
+    double2* base = buf + q * L + blk * st.B + s;
+    double2 v[R];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int b = b0 + u * NT;
-      ob[u] = -1;
-      if (b < total) {
-        const int s = fdiv(b, ps.mag_nbf);
-        const int j = b - s * nbf;
-        const int jq = fdiv(j, ps.mag_ns);
-        const int k = j - jq * Ns;
-        const double2* ip = in + s * L + j;
+    for (int r = 0; r < R; ++r) v[r] = base[r * S];
+    double2 w1 = make_double2(1.0, 0.0);
+    const bool twd = tw && s > 0;
+    if (twd) {
+      const int e = s * st.tmul;
+      w1 = cmul(tw2[kTwLo + (e >> 6)], tw2[e & (kTwLo - 1)]);
+    }
+    if (!kFwd && twd) {
+      double2 wr = w1;
+      v[1] = cmul(v[1], w1);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[u][r] = ip[r * nbf];
-        ob[u] = s * L + jq * Ns * R + k;
-        kk[u] = jq * Ns * R + k;
-        if (Ns > 1) {
-          // base twiddle from the two-level table in shared memory, powers by recurrence
-          const int e = k * ps.tstride;
-          const double2 w1 = cmul(W[kTwLo + (e >> 6)], W[e & (kTwLo - 1)]);
-          double2 wr = w1;
-          v[u][1] = cmul(v[u][1], w1);
-#pragma unroll
-          for (int r = 2; r < R; ++r) {
-            wr = cmul(wr, w1);
-            v[u][r] = cmul(v[u][r], wr);
-          }
-        }
+      for (int r = 2; r < R; ++r) {
+        wr = cmul(wr, w1);
+        v[r] = cmul(v[r], wr);
       }
     }
+    dft<R>(v);
+    if (kFwd && twd) {
+      double2 wr = w1;
+      v[1] = cmul(v[1], w1);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (ob[u] >= 0) {
-        dft<R>(v[u]);
-        double2* op = out + ob[u];
-        if (kPost) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) op[r * Ns] = conjc(cmul(v[u][r], __ldg(bhat + kk[u] + r * Ns)));
-        } else {
-#pragma unroll
-          for (int r = 0; r < R; ++r) op[r * Ns] = v[u][r];
-        }
+      for (int r = 2; r < R; ++r) {
+        wr = cmul(wr, w1);
+        v[r] = cmul(v[r], wr);
       }
+    }
+    if (kPost) {  // last DIT step: S == 1, positions blk * R + r
+      const double2* bh = bhat + blk * R;
+#pragma unroll
+      for (int r = 0; r < R; ++r) base[r] = conjc(cmul(v[r], __ldg(bh + r)));
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) base[r * S] = v[r];
     }
   }
   __syncthreads();
 }
 
-template <int V, bool kPost>
-__device__ __forceinline__ void pass_dispatch(const double2* in, double2* out, int nseq, int L, const FftPass& ps,
-                                              const double2* __restrict__ W, const double2* __restrict__ bhat) {
-  switch (ps.radix) {
-#define SHT_CASE(R)                                                                   \
-  case R:                                                                             \
-    if constexpr (FftCfg<V>::template has<R>()) pass_run<R, V, kPost>(in, out, nseq, L, ps, W, bhat); \
+template <int V, bool kFwd, bool kPost>
+__device__ __forceinline__ void step_dispatch(double2* buf, int nseq, int L, const FftStep& st, bool tw,
+                                              const double2* __restrict__ tw2, const double2* __restrict__ bhat) {
+  switch (st.R) {
+#define SHT_CASE(R)                                                                                  \
+  case R:                                                                                            \
+    if constexpr (FftCfg<V>::template has<R>()) step_run<R, V, kFwd, kPost>(buf, nseq, L, st, tw, tw2, bhat); \
     break;
     SHT_CASE(2) SHT_CASE(3) SHT_CASE(4) SHT_CASE(5) SHT_CASE(6) SHT_CASE(7) SHT_CASE(8) SHT_CASE(9)
     SHT_CASE(10) SHT_CASE(11) SHT_CASE(12) SHT_CASE(13) SHT_CASE(14) SHT_CASE(15) SHT_CASE(16)
     default:
-      if constexpr (FftCfg<V>::kBig) {
-        switch (ps.radix) { SHT_CASE(17) SHT_CASE(19) SHT_CASE(23) SHT_CASE(29) SHT_CASE(31) default: break; }
+      if constexpr (V == 2) {
+        switch (st.R) { SHT_CASE(17) SHT_CASE(19) SHT_CASE(23) SHT_CASE(29) SHT_CASE(31) default: break; }
       }
       break;
 #undef SHT_CASE
   }
 }
 
-// The ring DFT of nseq sequences held in a (b: scratch of the same size):
-// direct mixed radix, or Bluestein (FFT with the kernel product fused into
-// its last pass, then a second FFT).  Returns the buffer holding the result
-// (for Bluestein the conjugate of the convolution, see the callers).
+// The ring DFT of nseq sequences in buf (natural order in).  Direct: DIT,
+// spectrum left digit-reversed.  Bluestein: DIT with conj(X bhat) fused into
+// the last step, then the transposed FFT: buf holds conj(conv) in natural order.
 template <int V>
-__device__ __forceinline__ double2* ring_dft(double2* a, double2* b, int L, int nseq, const FftPass* passes,
-                                             int npass, const double2* __restrict__ W, bool blue,
-                                             const double2* __restrict__ bhat) {
-  const int nrun = blue ? 2 * npass : npass;
-  for (int t = 0; t < nrun; ++t) {
-    const FftPass& ps = passes[t < npass ? t : t - npass];
-    if (blue && t == npass - 1)
-      pass_dispatch<V, true>(a, b, nseq, L, ps, W, bhat);
+__device__ __forceinline__ void ring_dft(double2* buf, int L, int nseq, const FftStep* steps, int nstep,
+                                         const double2* __restrict__ tw2, bool blue,
+                                         const double2* __restrict__ bhat) {
+  for (int j = 0; j < nstep; ++j) {
+    if (blue && j == nstep - 1)
+      step_dispatch<V, true, true>(buf, nseq, L, steps[j], false, tw2, bhat);
     else
-      pass_dispatch<V, false>(a, b, nseq, L, ps, W, bhat);
-    double2* x = a;
-    a = b;
-    b = x;
+      step_dispatch<V, true, false>(buf, nseq, L, steps[j], j < nstep - 1, tw2, bhat);
   }
-  return a;
+  if (blue)
+    for (int j = nstep - 1; j >= 0; --j) step_dispatch<V, false, false>(buf, nseq, L, steps[j], j < nstep - 1, tw2, bhat);
 }
 
-// Shared prologue: ring descriptor + passes into shared memory.
+// Digit-reversed position of spectrum index k after the DIT steps.
+__device__ __forceinline__ int dit_pos(int k, const FftStep* steps, int nstep) {
+  int pos = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxSteps; ++j) {
+    if (j < nstep) {
+      const int kq = fdiv(k, steps[j].mag_R);
+      pos += (k - kq * steps[j].R) * steps[j].S;
+      k = kq;
+    }
+  }
+  return pos;
+}
+
+// Shared prologue: ring descriptor, steps and the 2-level twiddle table.
 struct RingSmem {
   FftRing rg;
-  FftPass ps[kMaxPasses];
-  double2 tw[kTwLo + kTwHi];  // two-level twiddle table of this ring's transform length
+  FftWork wk;
+  FftStep st[kMaxSteps];
+  double2 tw[kTwLo + kTwHi];
 };
 
-__device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, const FftWork& wk) {
-  if (threadIdx.x == 0) rs.rg = p.rings[wk.ring];
+__device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, int w) {
+  if (threadIdx.x == 0) {
+    rs.wk = p.work[w];
+    rs.rg = p.rings[rs.wk.ring];
+  }
   __syncthreads();
-  if ((int)threadIdx.x < rs.rg.npass) rs.ps[threadIdx.x] = p.passes[rs.rg.pass0 + threadIdx.x];
+  if ((int)threadIdx.x < rs.rg.nstep) rs.st[threadIdx.x] = p.steps[rs.rg.step0 + threadIdx.x];
   const int ntw = kTwLo + (rs.rg.L + kTwLo - 1) / kTwLo;
   for (int t = threadIdx.x; t < ntw; t += blockDim.x) rs.tw[t] = p.tw[rs.rg.tw2_off + t];
   __syncthreads();
+}
+
+// Batches: nb == 2K -> K field pairs, sequence q = 2 pl + side; nb == 1 -> one
+// sequence per batch: north then south of each field pair.
+struct Batch {
+  int pa, npr, nseq;   // first field pair, pairs, sequences
+  int side;            // nb == 1: hemisphere of the single sequence
+};
+
+__device__ __forceinline__ Batch batch_of(const FftRing& rg, const FftWork& wk, int t) {
+  Batch b;
+  if (rg.nb > 1) {
+    b.pa = wk.fp0 + t * rg.K;
+    b.npr = min(rg.K, wk.fp1 - b.pa);
+    b.nseq = 2 * b.npr;
+    b.side = -1;
+  } else {
+    b.pa = wk.fp0 + (t >> 1);
+    b.npr = 1;
+    b.nseq = 1;
+    b.side = t & 1;
+  }
+  return b;
 }
 
 // ------------------------------------------------------------------ grid -> Fourier
@@ -195,33 +225,26 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   constexpr int NT = FftCfg<V>::kThreads;
   extern __shared__ __align__(16) double2 smc[];
   __shared__ RingSmem rs;
-  const FftWork wk = p.work[w0 + blockIdx.x];
-  load_ring(rs, p, wk);
+  load_ring(rs, p, w0 + blockIdx.x);
   const FftRing& rg = rs.rg;
   const int N = rg.n, L = rg.L, M = rg.mcap;
-  const int npairs = (p.nfld + 1) / 2;
-  const int nfp = min(rg.fp, npairs - wk.fp0);
-  const int nseq = 2 * nfp;  // sequence q: side = q / nfp (0 north, 1 south), field pair q % nfp
-  const int nb = rg.nb;
   double2* buf = smc;
-  double2* buf2 = smc + (size_t)nb * L;
-  double2* stg = buf2 + (size_t)nb * L;  // northern F^a, F^b: [m][2 nfp]
+  double2* stg = smc + (size_t)rg.nb * L;  // nb == 1: northern F^a, F^b of the current pair, [m][2]
   const bool blue = rg.chirp_off >= 0;
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
   const double scale = 0.5 / N;
-  const int nf = min(2 * nfp, p.nfld - 2 * wk.fp0);
   const int64_t rowd = (int64_t)p.nfld * 4;
   const double w = rg.w;
+  const int nbatch = rg.nb > 1 ? (rs.wk.fp1 - rs.wk.fp0 + rg.K - 1) / rg.K : 2 * (rs.wk.fp1 - rs.wk.fp0);
 
-  for (int q0 = 0; q0 < nseq; q0 += nb) {
-    const int nq = min(nb, nseq - q0);
-    // grid -> smem with cp.async (field a -> .x, field b -> .y); zero tail / missing field
-    for (int idx = threadIdx.x; idx < nq * L; idx += NT) {
-      const int ql = fdiv(idx, rg.mag_L), n = idx - ql * L;
-      const int q = q0 + ql;
-      const int side = q >= nfp, pr = q - side * nfp;
-      const int fa = 2 * (wk.fp0 + pr);
+  for (int t = 0; t < nbatch; ++t) {
+    const Batch bt = batch_of(rg, rs.wk, t);
+    // grid -> smem (cp.async, field a -> .x, field b -> .y), zero tail, chirp
+    for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
+      const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
+      const int fa = 2 * (bt.pa + (bt.side < 0 ? (q >> 1) : 0));
+      const int side = bt.side < 0 ? (q & 1) : bt.side;
       double* dst = reinterpret_cast<double*>(buf + idx);
       if (n < N) {
         const int64_t go = (side ? rg.goff_s : rg.goff_n) + n;
@@ -234,53 +257,64 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
         buf[idx] = make_double2(0.0, 0.0);
       }
     }
-    cp_async_wait_all();
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     if (blue) {
-      for (int idx = threadIdx.x; idx < nq * L; idx += NT) {
-        const int ql = fdiv(idx, rg.mag_L), n = idx - ql * L;
+      for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
+        const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
         if (n < N) buf[idx] = cmul(buf[idx], __ldg(chirp + n));
       }
       __syncthreads();
     }
-    const double2* res = (p.debug & 1) ? buf : ring_dft<V>(buf, buf2, L, nq, rs.ps, rg.npass, rs.tw, blue, bhat);
-    // extract F^a_m, F^b_m: northern sequences are staged first, southern ones
-    // then complete the parity rows S' = w (F_N + F_S), A' = w (F_N - F_S)
-    for (int side = 0; side < 2; ++side) {
-      const int qa = max(q0, side * nfp), qb = min(q0 + nq, (side + 1) * nfp);
-      if (qa < qb) {
-        for (int idx = threadIdx.x; idx < (qb - qa) * (M + 1); idx += NT) {
-          const int qq = fdiv(idx, rg.mag_M1), m = idx - qq * (M + 1);
-          const int q = qa + qq, ql = q - q0;
-          const int pr = q - side * nfp;
-          const int k2 = (m == 0) ? 0 : N - m;
-          double2 zm = res[ql * L + m], zn = res[ql * L + k2];
-          if (blue) {
-            zm = cmul(__ldg(chirp + m), conjc(zm));
-            zn = cmul(__ldg(chirp + k2), conjc(zn));
-          }
-          const double2 fa = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);
-          const double2 fb = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);
-          double2* st = stg + (size_t)m * (2 * nfp) + 2 * pr;
-          if (!side) {
-            st[0] = fa;
-            st[1] = fb;
-          } else {
-            const int f = 2 * pr;
-            const int64_t row = p.yrow[rg.yrow_off + m];
-            double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)(2 * wk.fp0 + f) * 4);
-            const double2 na = st[0], nbv = st[1];
-            __stcs(d, make_double2(w * (na.x + fa.x), w * (na.y + fa.y)));
-            __stcs(d + 1, make_double2(w * (na.x - fa.x), w * (na.y - fa.y)));
-            if (f + 1 < nf) {
-              __stcs(d + 2, make_double2(w * (nbv.x + fb.x), w * (nbv.y + fb.y)));
-              __stcs(d + 3, make_double2(w * (nbv.x - fb.x), w * (nbv.y - fb.y)));
-            }
+    if (!(p.debug & 1)) ring_dft<V>(buf, L, bt.nseq, rs.st, rg.nstep, rs.tw, blue, bhat);
+    auto Z = [&](int q, int k) {
+      if (blue) return cmul(__ldg(chirp + k), conjc(buf[q * L + k]));
+      return buf[q * L + dit_pos(k, rs.st, rg.nstep)];
+    };
+    auto split = [&](int q, int m, double2& fa, double2& fb) {
+      const double2 zm = Z(q, m), zn = Z(q, m == 0 ? 0 : N - m);
+      fa = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);
+      fb = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);
+    };
+    if (bt.side < 0) {
+      for (int idx = threadIdx.x; idx < bt.npr * (M + 1); idx += NT) {
+        const int m = idx / bt.npr, pl = idx - m * bt.npr;
+        double2 na, nbv, sa, sb;
+        split(2 * pl, m, na, nbv);
+        split(2 * pl + 1, m, sa, sb);
+        const int fa = 2 * (bt.pa + pl);
+        const int64_t row = p.yrow[rg.yrow_off + m];
+        double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
+        __stcs(d, make_double2(w * (na.x + sa.x), w * (na.y + sa.y)));
+        __stcs(d + 1, make_double2(w * (na.x - sa.x), w * (na.y - sa.y)));
+        if (fa + 1 < p.nfld) {
+          __stcs(d + 2, make_double2(w * (nbv.x + sb.x), w * (nbv.y + sb.y)));
+          __stcs(d + 3, make_double2(w * (nbv.x - sb.x), w * (nbv.y - sb.y)));
+        }
+      }
+    } else {
+      const int fa = 2 * bt.pa;
+      for (int m = threadIdx.x; m <= M; m += NT) {
+        double2 xa, xb;
+        split(0, m, xa, xb);
+        if (bt.side == 0) {
+          stg[2 * m] = xa;
+          stg[2 * m + 1] = xb;
+        } else {
+          const double2 na = stg[2 * m], nbv = stg[2 * m + 1];
+          const int64_t row = p.yrow[rg.yrow_off + m];
+          double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
+          __stcs(d, make_double2(w * (na.x + xa.x), w * (na.y + xa.y)));
+          __stcs(d + 1, make_double2(w * (na.x - xa.x), w * (na.y - xa.y)));
+          if (fa + 1 < p.nfld) {
+            __stcs(d + 2, make_double2(w * (nbv.x + xb.x), w * (nbv.y + xb.y)));
+            __stcs(d + 3, make_double2(w * (nbv.x - xb.x), w * (nbv.y - xb.y)));
           }
         }
-        __syncthreads();
       }
     }
+    __syncthreads();
   }
 }
 
@@ -291,77 +325,67 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   constexpr int NT = FftCfg<V>::kThreads;
   extern __shared__ __align__(16) double2 smc[];
   __shared__ RingSmem rs;
-  const FftWork wk = p.work[w0 + blockIdx.x];
-  load_ring(rs, p, wk);
+  load_ring(rs, p, w0 + blockIdx.x);
   const FftRing& rg = rs.rg;
   const int N = rg.n, L = rg.L, M = rg.mcap;
-  const int npairs = (p.nfld + 1) / 2;
-  const int nfp = min(rg.fp, npairs - wk.fp0);
-  const int nseq = 2 * nfp;
-  const int nb = rg.nb;
   double2* buf = smc;
-  double2* buf2 = smc + (size_t)nb * L;
   const bool blue = rg.chirp_off >= 0;
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
   const int64_t rowd = (int64_t)p.nfld * 4;
-  const int nf = min(2 * nfp, p.nfld - 2 * wk.fp0);
-  double2* stg = buf2 + (size_t)nb * L;  // rows of this CTA's fields: [m][f][S, A]
-  {
-    const int chunks = 2 * nf;  // 16-byte chunks per row
-    for (int idx = threadIdx.x; idx < (M + 1) * chunks; idx += NT) {
-      const int m = idx / chunks, c = idx - m * chunks;
-      const int64_t row = p.yrow[rg.yrow_off + m];
-      cp_async16(stg + (size_t)m * (4 * nfp) + c, four + row * rowd + (int64_t)(2 * wk.fp0) * 4 + 2 * c);
-    }
-    if (nf < 2 * nfp)  // odd field count: zero the missing field's slots
-      for (int m = threadIdx.x; m <= M; m += NT) {
-        stg[(size_t)m * (4 * nfp) + 2 * nf] = make_double2(0.0, 0.0);
-        stg[(size_t)m * (4 * nfp) + 2 * nf + 1] = make_double2(0.0, 0.0);
-      }
-    cp_async_wait_all();
-    __syncthreads();
-  }
+  const int nbatch = rg.nb > 1 ? (rs.wk.fp1 - rs.wk.fp0 + rg.K - 1) / rg.K : 2 * (rs.wk.fp1 - rs.wk.fp0);
 
-  for (int q0 = 0; q0 < nseq; q0 += nb) {
-    const int nq = min(nb, nseq - q0);
-    for (int idx = threadIdx.x; idx < nq * L; idx += NT) {
-      const int ql = fdiv(idx, rg.mag_L), k = idx - ql * L;
-      const int q = q0 + ql;
-      const int side = q >= nfp, pr = q - side * nfp;
-      double2 z = make_double2(0.0, 0.0);
-      int m = -1;
-      bool lo = true;
-      if (k <= M) {
-        m = k;
-      } else if (k < N && k >= N - M) {
-        m = N - k;
-        lo = false;
+  for (int t = 0; t < nbatch; ++t) {
+    const Batch bt = batch_of(rg, rs.wk, t);
+    // zero the bins no coefficient reaches: (M, N-M) and [N, L)
+    const int gap = (N - 2 * M - 1) + (L - N);
+    for (int idx = threadIdx.x; idx < bt.nseq * gap; idx += NT) {
+      const int q = idx / gap, g = idx - q * gap;
+      const int k = g < N - 2 * M - 1 ? M + 1 + g : N + (g - (N - 2 * M - 1));
+      buf[q * L + k] = make_double2(0.0, 0.0);
+    }
+    // Fourier rows -> conj(Z) of both hemispheres at k = m and k = N - m
+    // (one thread per (m, field pair): a row's 64-byte chunks are read once)
+    for (int idx = threadIdx.x; idx < bt.npr * (M + 1); idx += NT) {
+      const int m = idx / bt.npr, pl = idx - m * bt.npr;
+      const int fa = 2 * (bt.pa + pl);
+      const int64_t row = p.yrow[rg.yrow_off + m];
+      const double2* src = reinterpret_cast<const double2*>(four + row * rowd + (int64_t)fa * 4);
+      const double2 sa = __ldcs(src), aa = __ldcs(src + 1);
+      double2 sb = make_double2(0.0, 0.0), ab = sb;
+      if (fa + 1 < p.nfld) {
+        sb = __ldcs(src + 2);
+        ab = __ldcs(src + 3);
       }
-      if (m >= 0) {
-        const double2* src = stg + (size_t)m * (4 * nfp) + 4 * pr;
-        const double2 sa = src[0], aa = src[1], sb = src[2], ab = src[3];
+      for (int side = 0; side < 2; ++side) {
+        if (bt.side >= 0 && side != bt.side) continue;
+        const int q = bt.side >= 0 ? 0 : 2 * pl + side;
         double2 Fa = side ? csub(sa, aa) : cadd(sa, aa);
         double2 Fb = side ? csub(sb, ab) : cadd(sb, ab);
         if (m == 0) {
           Fa.y = 0.0;
           Fb.y = 0.0;
         }
-        // Z = Fa + i Fb (low half) or conj(Fa) + i conj(Fb) (mirror half); feed conj(Z)
-        z = lo ? make_double2(Fa.x - Fb.y, -(Fa.y + Fb.x)) : make_double2(Fa.x + Fb.y, Fa.y - Fb.x);
-        if (blue) z = cmul(z, __ldg(chirp + k));
+        // conj(Z) at k = m (Z = Fa + i Fb) and at k = N - m (Z = conj(Fa) + i conj(Fb))
+        double2 lo = make_double2(Fa.x - Fb.y, -(Fa.y + Fb.x));
+        double2 hi = make_double2(Fa.x + Fb.y, Fa.y - Fb.x);
+        if (blue) {
+          lo = cmul(lo, __ldg(chirp + m));
+          if (m) hi = cmul(hi, __ldg(chirp + N - m));
+        }
+        buf[q * L + m] = lo;
+        if (m) buf[q * L + N - m] = hi;
       }
-      buf[idx] = z;
     }
     __syncthreads();
-    const double2* res = (p.debug & 1) ? buf : ring_dft<V>(buf, buf2, L, nq, rs.ps, rg.npass, rs.tw, blue, bhat);
-    for (int idx = threadIdx.x; idx < nq * N; idx += NT) {
-      const int ql = fdiv(idx, rg.mag_N), k = idx - ql * N;
-      const int q = q0 + ql;
-      const int side = q >= nfp, pr = q - side * nfp;
-      double2 r = res[ql * L + k];
-      if (blue) r = cmul(__ldg(chirp + k), conjc(r));
-      const int fa = 2 * (wk.fp0 + pr);
+    if (!(p.debug & 1)) ring_dft<V>(buf, L, bt.nseq, rs.st, rg.nstep, rs.tw, blue, bhat);
+    for (int idx = threadIdx.x; idx < bt.nseq * N; idx += NT) {
+      const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
+      const int pl = bt.side >= 0 ? 0 : (q >> 1);
+      const int side = bt.side >= 0 ? bt.side : (q & 1);
+      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[q * L + k]))
+                             : buf[q * L + dit_pos(k, rs.st, rg.nstep)];
+      const int fa = 2 * (bt.pa + pl);
       const int64_t go = (side ? rg.goff_s : rg.goff_n) + k;
       __stcs(grid + (int64_t)fa * p.grid_ld + go, r.x);
       if (fa + 1 < p.nfld) __stcs(grid + (int64_t)(fa + 1) * p.grid_ld + go, -r.y);
@@ -387,19 +411,8 @@ static void launch_one(bool g2f, const FftParams& p, int w0, int nw, const doubl
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s) {
   if (nw <= 0) return;
-  if (variant == 0) launch_one<0>(g2f, p, w0, nw, in, out, smem, s);
   if (variant == 1) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
   if (variant == 2) launch_one<2>(g2f, p, w0, nw, in, out, smem, s);
-}
-
-int fft_variant_threads(int variant) {
-  return variant == 0 ? FftCfg<0>::kThreads : variant == 1 ? FftCfg<1>::kThreads : FftCfg<2>::kThreads;
-}
-
-int fft_capacity(int variant, const std::vector<int>& radices) {
-  (void)variant;
-  (void)radices;
-  return kFftMaxLen;  // ping-pong passes loop over butterflies: only shared memory bounds a batch
 }
 
 // ------------------------------------------------------------------ host-side planning
@@ -414,19 +427,18 @@ static bool factor_primes(int n, int maxp, std::vector<int>& primes) {
   return m == 1;
 }
 
-// Group prime factors into passes: primes > 16 alone, the rest packed into
-// composite radices <= 16 (first-fit decreasing on the product); odd radices
-// first so the stride-R writes of the first pass hit distinct banks.
-static void group_passes(std::vector<int> primes, std::vector<int>& radices, int cap) {
+// Pencil radices: primes > 16 alone, the rest multiplied into factors <= 16
+// (first-fit decreasing), as few steps as possible.
+static void group_pencils(const std::vector<int>& primes, std::vector<int>& radices) {
   radices.clear();
   std::vector<int> small;
-  for (int p : primes) (p > cap ? radices : small).push_back(p);
+  for (int p : primes) (p > 16 ? radices : small).push_back(p);
   std::sort(small.begin(), small.end(), std::greater<int>());
   std::vector<int> bins;
   for (int p : small) {
     bool placed = false;
     for (int& b : bins)
-      if (b * p <= cap) {
+      if (b * p <= 16) {
         b *= p;
         placed = true;
         break;
@@ -434,25 +446,26 @@ static void group_passes(std::vector<int> primes, std::vector<int>& radices, int
     if (!placed) bins.push_back(p);
   }
   radices.insert(radices.end(), bins.begin(), bins.end());
-  std::stable_sort(radices.begin(), radices.end(), [](int a, int b) { return (a & 1) > (b & 1); });
+  if (radices.empty()) radices.push_back(1);
 }
 
-int fft_choose(int n, int cap, std::vector<int>& radices, int& L, bool& bluestein) {
+int fft_choose(int n, int& variant, std::vector<int>& radices, int& L, bool& bluestein) {
   std::vector<int> primes;
-  const int maxp = cap >= 16 ? 31 : 13;
-  if (n >= 1 && factor_primes(n, maxp, primes)) {
-    group_passes(primes, radices, cap);
-    if ((int)radices.size() <= kMaxPasses && n <= kFftMaxLen) {
+  bluestein = false;
+  if (n >= 2 && n <= kFftMaxLen && factor_primes(n, 31, primes)) {
+    group_pencils(primes, radices);
+    if ((int)radices.size() <= kMaxSteps) {
+      variant = *std::max_element(radices.begin(), radices.end()) > 16 ? 2 : 1;
       L = n;
-      bluestein = false;
       return 0;
     }
   }
   bluestein = true;
   for (int cand = 2 * n - 1; cand <= kFftMaxLen; ++cand) {
-    if (factor_primes(cand, cap >= 16 ? 13 : 7, primes)) {
-      group_passes(primes, radices, cap);
-      if ((int)radices.size() <= kMaxPasses) {
+    if (factor_primes(cand, 13, primes)) {
+      group_pencils(primes, radices);
+      if ((int)radices.size() <= kMaxSteps) {
+        variant = 1;
         L = cand;
         return 0;
       }
@@ -461,31 +474,35 @@ int fft_choose(int n, int cap, std::vector<int>& radices, int& L, bool& bluestei
   return SHT_ERR_CONFIG;
 }
 
-int fft_choose(int n, std::vector<int>& radices, int& L, bool& bluestein) {
-  return fft_choose(n, 16, radices, L, bluestein);
-}
-
-bool fft_needs_big(const std::vector<int>& radices) {
-  for (int r : radices)
-    if (r > 16) return true;
-  return false;
-}
-
-void fft_passes(int L, const std::vector<int>& radices, std::vector<FftPass>& out, std::vector<double2>& arena,
-                int64_t& tw2_off) {
-  const long double two_pi = 6.283185307179586476925286766559005768L;
-  int Ns = 1;
+int fft_pos(int k, const std::vector<int>& radices) {
+  int S = 1;
+  for (int R : radices) S *= R;
+  int pos = 0;
   for (int R : radices) {
-    FftPass ps;
-    ps.radix = R;
-    ps.ns = Ns;
-    ps.nbf = L / R;
-    ps.mag_nbf = ((uint64_t)1 << 40) / (uint64_t)ps.nbf + 1;
-    ps.mag_ns = ((uint64_t)1 << 40) / (uint64_t)Ns + 1;
-    ps.tstride = L / (Ns * R);
-    ps.pad = ps.pad2 = 0;
-    out.push_back(ps);
-    Ns *= R;
+    S /= R;
+    pos += (k % R) * S;
+    k /= R;
+  }
+  return pos;
+}
+
+void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
+               int64_t& tw2_off) {
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  int B = L;
+  for (int R : radices) {
+    FftStep st;
+    st.R = R;
+    st.B = B;
+    st.S = B / R;
+    st.np = L / R;
+    st.tmul = L / B;
+    st.pad = 0;
+    st.mag_S = ((uint64_t)1 << 40) / (uint64_t)st.S + 1;
+    st.mag_np = ((uint64_t)1 << 40) / (uint64_t)st.np + 1;
+    st.mag_R = ((uint64_t)1 << 40) / (uint64_t)R + 1;
+    out.push_back(st);
+    B = st.S;
   }
   tw2_off = (int64_t)arena.size();
   auto W = [&](long long e) {

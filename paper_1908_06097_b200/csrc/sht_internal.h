@@ -65,35 +65,35 @@ size_t leg_inv_smem();
 size_t leg_dir_smem();
 
 // ---------------------------------------------------------------- ring FFTs
-constexpr int kMaxPasses = 8;
-constexpr int kFftMaxLen = 6912;   // longest transform one CTA handles (ping-pong buffers in smem)
-
-struct FftPass {       // one Stockham pass of a ring plan
-  int32_t radix;
-  int32_t ns;          // span: product of the radices already applied
-  int32_t nbf;         // butterflies per sequence = L / radix
-  int32_t pad;
-  uint64_t mag_nbf;    // multiply-shift (>> 40) divisors for nbf and ns
-  uint64_t mag_ns;
-  int32_t tstride;     // L / (ns radix): base twiddle of butterfly k is W_L^(k tstride)
-  int32_t pad2;
-};
-
+constexpr int kMaxSteps = 4;
+constexpr int kFftMaxLen = 6912;                   // longest transform one CTA handles
 constexpr int kTwLo = 64;                          // two-level twiddle table: W_L^e = hi[e / 64] lo[e % 64]
-constexpr int kTwHi = (6912 + kTwLo - 1) / kTwLo;  // entries of hi for the longest transform
+constexpr int kTwHi = (kFftMaxLen + kTwLo - 1) / kTwLo;
+
+// One step of the in-place "pencil" FFT of length L = R_0 R_1 ... R_{d-1}:
+// blocks of length B = R_j S, each holding S pencils of R points at stride S.
+struct FftStep {
+  int32_t R;           // pencil length (radix)
+  int32_t S;           // pencil stride = B / R
+  int32_t B;           // block length
+  int32_t np;          // pencils per sequence = L / R
+  int32_t tmul;        // L / B: twiddle W_B^(r s) = W_L^(r s tmul)
+  int32_t pad;
+  uint64_t mag_S, mag_np, mag_R;  // multiply-shift (>> 40) divisors
+};
 
 struct FftRing {       // one northern ring (and its southern mirror) on this rank
   int32_t n;           // points on the ring
   int32_t L;           // transform length (n, or the Bluestein length)
   int32_t mcap;        // M_i
-  int32_t npass;
-  int32_t pass0;       // first pass in FftParams::passes
-  int32_t fp;          // field pairs per CTA
-  int32_t nb;          // sequences per FFT batch
-  int32_t pad;
+  int32_t nstep;
+  int32_t step0;       // first step in FftParams::steps
+  int32_t K;           // field pairs per batch
+  int32_t nb;          // sequences per batch: 2K (both hemispheres) or 1
+  int32_t variant;
   uint64_t mag_L, mag_N, mag_M1;  // multiply-shift (>> 40) divisors for L, n, mcap + 1
-  int64_t chirp_off;   // Bluestein chirp w_n = exp(-pi i n^2 / N), n < N   (-1: none)
-  int64_t bhat_off;    // Bluestein kernel spectrum / L                     (-1: none)
+  int64_t chirp_off;   // Bluestein chirp w_n = exp(-pi i n^2 / N), n < N            (-1: none)
+  int64_t bhat_off;    // Bluestein kernel spectrum / L, in the DIT output (digit-reversed) order
   int64_t goff_n;      // offset of the northern ring in the local grid field
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
@@ -101,36 +101,35 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   double w;            // Gaussian weight
 };
 
-struct FftWork {       // one CTA of a ring-FFT launch
-  int32_t ring;        // local ring index
-  int32_t fp0;         // first field pair
+struct FftWork {       // one CTA: field pairs [fp0, fp1) of one ring pair
+  int32_t ring;
+  int32_t fp0;
+  int32_t fp1;
+  int32_t pad;
 };
 
 struct FftParams {
   int nfld;
   int64_t grid_ld;           // doubles per local grid field
   const FftRing* rings;
-  const FftPass* passes;
+  const FftStep* steps;
   const FftWork* work;
   const double2* tw;         // twiddle / chirp arena
   const int32_t* yrow;       // Fourier row of (ring, m)
-  int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT passes
+  int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT steps
 };
 
-// Launch CTAs work[w0 .. w0+nw) of a ring-FFT class.  variant 0: radix <= 16,
-// 256 threads, 2 CTAs/SM; 1: radix <= 16, 512 threads; 2: prime radices up to
-// 31, 256 threads.  g2f: grid -> Fourier (in = grid), else Fourier -> grid.
+// Ring-FFT kernel variants: 1 = pencils <= 16 points, 256 threads, 2 CTAs/SM;
+// 2 = pencils up to 31 points (primes 17..31), 256 threads, 1 CTA/SM.
+constexpr int kFftVariants = 3;  // index 0 unused
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s);
-// Complex values one in-place pass of `variant` can hold for these radices.
-int fft_capacity(int variant, const std::vector<int>& radices);
-// Plan for a ring of n points: mixed radix (composite <= 16, primes <= 31)
-// when n factors over those, else Bluestein with a 13-smooth L >= 2n-1.
-int fft_choose(int n, std::vector<int>& radices, int& L, bool& bluestein);
-// Same with composite radices capped at `cap` (16, or 8 for the 1024-thread variant).
-int fft_choose(int n, int cap, std::vector<int>& radices, int& L, bool& bluestein);
-bool fft_needs_big(const std::vector<int>& radices);
-void fft_passes(int L, const std::vector<int>& radices, std::vector<FftPass>& out, std::vector<double2>& arena,
-                int64_t& tw2_off);
+// Plan for a ring of n points: kernel variant, pencil radices and transform
+// length (n, or a 13-smooth Bluestein length L >= 2n-1).
+int fft_choose(int n, int& variant, std::vector<int>& radices, int& L, bool& bluestein);
+void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
+               int64_t& tw2_off);
+// Position of DFT output k after the in-place DIT pencil FFT (digit reversal).
+int fft_pos(int k, const std::vector<int>& radices);
 
 }  // namespace sht

@@ -189,9 +189,9 @@ struct sht_plan {
   double* Y = nullptr;
   sht::FftRing* d_rings = nullptr;
   sht::FftWork* d_work = nullptr;
-  int fft_w0[3] = {0, 0, 0}, fft_nw[3] = {0, 0, 0};  // per ring-FFT kernel variant
-  size_t fft_smem[3] = {0, 0, 0};
-  sht::FftPass* d_passes = nullptr;
+  int fft_w0[sht::kFftVariants] = {}, fft_nw[sht::kFftVariants] = {};  // per ring-FFT kernel variant
+  size_t fft_smem[sht::kFftVariants] = {};
+  sht::FftStep* d_steps = nullptr;
   double2* d_tw = nullptr;
   int32_t* d_yrow = nullptr;
   ncclComm_t comm = nullptr;
@@ -211,7 +211,7 @@ namespace sht {
 static void free_plan(sht_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
-                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_passes,
+                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -355,9 +355,10 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   }
   p->grid_ld = go;
   const int npairs = (nfld + 1) / 2;
-  const size_t budget_small = 108 * 1024, budget_large = 220 * 1024;
-  std::vector<std::pair<int64_t, FftWork>> wcls[3];  // per kernel variant
-  std::vector<FftPass> passes;
+  // shared memory per CTA: variant 1 runs 2 CTAs/SM, variant 2 one
+  const size_t budget[kFftVariants] = {0, 108 * 1024, 216 * 1024};
+  std::vector<FftStep> steps;
+  std::vector<int64_t> ring_cost(nlr, 0);
   int64_t nfour_local = 0;
   for (int lr = 0; lr < nlr; ++lr) {
     const int i = p->my_rings[lr];
@@ -367,28 +368,18 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     R.w = p->w[i];
     nfour_local += 2 * (int64_t)(R.mcap + 1);
     std::vector<int> rad;
-    int L = 0;
+    int L = 0, variant = 0;
     bool blue = false;
-    if (fft_choose(R.n, 16, rad, L, blue))
+    if (fft_choose(R.n, variant, rad, L, blue))
       return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
-    // variant: 2 if a prime radix > 16 is needed; 0 if a 256-thread CTA fits in
-    // ~108 KB (2 CTAs/SM); else 1 (1024 threads, radices <= 8)
-    int variant = fft_needs_big(rad) ? 2 : 0;
-    if (variant == 0) {
-      const size_t one = (2 * (size_t)std::min(2, 2 * npairs) * L + 4 * (size_t)(g.mcap[i] + 1)) * sizeof(double2);
-      if (one > budget_small) {
-        variant = 1;
-        if (fft_choose(R.n, 8, rad, L, blue))
-          return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
-      }
-    }
     R.L = L;
+    R.variant = variant;
     R.mag_L = ((uint64_t)1 << 40) / (uint64_t)L + 1;
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
-    R.npass = (int)rad.size();
-    R.pass0 = (int)passes.size();
-    fft_passes(L, rad, passes, arena, R.tw2_off);
+    R.nstep = (int)rad.size();
+    R.step0 = (int)steps.size();
+    fft_steps(L, rad, steps, arena, R.tw2_off);
     const long double pi_ld = 3.14159265358979323846264338327950288L;
     R.chirp_off = R.bhat_off = -1;
     if (blue) {
@@ -408,11 +399,14 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
           if (n) b[L - n] = std::conj(chirp[n]);
         }
         dft_rec(b.data(), 1, bh.data(), L);
-        bhat_of_N[N] = (int64_t)arena.size();
+        // stored in the digit-reversed order the DIT steps leave the spectrum in
+        std::vector<double2> perm(L);
         for (int k = 0; k < L; ++k) {
           const cld v = bh[k] / (long double)L;
-          arena.push_back(make_double2((double)v.real(), (double)v.imag()));
+          perm[fft_pos(k, rad)] = make_double2((double)v.real(), (double)v.imag());
         }
+        bhat_of_N[N] = (int64_t)arena.size();
+        arena.insert(arena.end(), perm.begin(), perm.end());
       }
       R.chirp_off = chirp_of_N[N];
       R.bhat_off = bhat_of_N[N];
@@ -422,44 +416,52 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
       const int s = p->m_owner[m];
       yrow.push_back((int32_t)(ybase[s][i] + p->lm_of_m[m]));
     }
-    // kernel variant, field pairs per CTA (fp) and sequences per FFT batch (nb):
-    // ping + pong buffers of nb sequences + a staging area of (M+1) rows x 2fp
-    // fields x {S, A}; prefer one batch (nb = 2 fp) and as many fields as fit.
-    auto smem = [&](int fp, int nb) { return (2 * (size_t)nb * L + 4 * (size_t)(R.mcap + 1) * fp) * sizeof(double2); };
-    auto pick = [&](int variant, size_t budget, int& fpo, int& nbo) {
-      const int nbmax = fft_capacity(variant, rad) / L;
-      if (nbmax < 1) return false;
-      for (int fp = std::min(npairs, 64); fp >= 1; --fp) {
-        const int nb = std::min(nbmax, 2 * fp);
-        if (nb == 2 * fp && smem(fp, nb) <= budget) {
-          fpo = fp;
-          nbo = nb;
-          return true;
+    // batch: K field pairs with both hemispheres (nb = 2K sequences of L) when
+    // they fit, else one sequence at a time (nb = 1; g2f stages the northern
+    // coefficients, (M+1) x 2 complex)
+    auto smem = [&](int nb) {
+      return ((size_t)nb * L + (nb == 1 ? 2 * (size_t)(R.mcap + 1) : 0)) * sizeof(double2);
+    };
+    int K = std::min(npairs, 64), nb = 2 * K;
+    while (K > 1 && smem(2 * K) > budget[variant]) nb = 2 * --K;
+    if (smem(nb) > budget[variant]) nb = 1;
+    if (smem(nb) > budget[variant])
+      return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+    R.K = K;
+    R.nb = nb;
+    p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb));
+    ring_cost[lr] = (int64_t)npairs * (2LL * L * R.nstep * (blue ? 2 : 1) + 8LL * R.n);
+  }
+  // split every ring's field pairs over CTAs so each variant's launch has
+  // ~6 CTAs per SM of balanced cost; largest first (LPT)
+  std::vector<FftWork> work;
+  {
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    for (int v = 1; v < kFftVariants; ++v) {
+      int64_t tot = 0;
+      for (int lr = 0; lr < nlr; ++lr)
+        if (rings[lr].variant == v) tot += ring_cost[lr];
+      std::vector<std::pair<int64_t, FftWork>> wl;
+      const double target = std::max<double>(1.0, (double)tot / (6.0 * nsm));
+      for (int lr = 0; lr < nlr; ++lr) {
+        if (rings[lr].variant != v) continue;
+        const int K = rings[lr].nb > 1 ? rings[lr].K : 1;
+        const int maxsplit = (npairs + K - 1) / K;
+        const int splits = std::max(1, std::min(maxsplit, (int)std::llround(ring_cost[lr] / target)));
+        int chunk = (npairs + splits - 1) / splits;
+        chunk = (chunk + K - 1) / K * K;
+        for (int a = 0; a < npairs; a += chunk) {
+          const int b = std::min(npairs, a + chunk);
+          wl.push_back({ring_cost[lr] * (b - a) / npairs, {lr, a, b, 0}});
         }
       }
-      if (smem(1, 1) <= budget) {  // one sequence at a time (north, then south)
-        fpo = 1;
-        nbo = 1;
-        return true;
-      }
-      return false;
-    };
-    int fp = 0, nb = 0;
-    if (!pick(variant, variant == 0 ? budget_small : budget_large, fp, nb))
-      return fail(SHT_ERR_CONFIG, "ring FFT does not fit (N=" + std::to_string(R.n) + ")");
-    R.fp = fp;
-    R.nb = nb;
-    p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(fp, nb));
-    const int64_t cost = (int64_t)2 * fp * L * R.npass * (blue ? 2 : 1);
-    for (int fp0 = 0; fp0 < npairs; fp0 += fp) wcls[variant].push_back({cost, {lr, fp0}});
-  }
-  auto bycost = [](const std::pair<int64_t, FftWork>& a, const std::pair<int64_t, FftWork>& b) { return a.first > b.first; };
-  std::vector<FftWork> work;
-  for (int c : {1, 2, 0}) {  // 1-CTA/SM variants first, they carry the largest rings
-    std::stable_sort(wcls[c].begin(), wcls[c].end(), bycost);
-    p->fft_w0[c] = (int)work.size();
-    p->fft_nw[c] = (int)wcls[c].size();
-    for (auto& x : wcls[c]) work.push_back(x.second);
+      std::stable_sort(wl.begin(), wl.end(), [](const std::pair<int64_t, FftWork>& x,
+                                                const std::pair<int64_t, FftWork>& y) { return x.first > y.first; });
+      p->fft_w0[v] = (int)work.size();
+      p->fft_nw[v] = (int)wl.size();
+      for (auto& x : wl) work.push_back(x.second);
+    }
   }
   int64_t npts_local = go;
   p->work_fft = 2.0 * nfld * (8.0 * (double)npts_local + 16.0 * (double)nfour_local);
@@ -484,7 +486,7 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   if (int rc = upload(&p->d_tiles_dir, td)) return rc;
   if (int rc = upload(&p->d_rings, rings)) return rc;
   if (int rc = upload(&p->d_work, work)) return rc;
-  if (int rc = upload(&p->d_passes, passes)) return rc;
+  if (int rc = upload(&p->d_steps, steps)) return rc;
   if (int rc = upload(&p->d_tw, arena)) return rc;
   if (int rc = upload(&p->d_yrow, yrow)) return rc;
   SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
@@ -555,7 +557,7 @@ static FftParams fft_params(const sht_plan* p) {
   fp.nfld = p->nfld;
   fp.grid_ld = p->grid_ld;
   fp.rings = p->d_rings;
-  fp.passes = p->d_passes;
+  fp.steps = p->d_steps;
   fp.work = p->d_work;
   fp.tw = p->d_tw;
   fp.yrow = p->d_yrow;
@@ -653,10 +655,10 @@ int sht_alltoall_order(int nranks, int rank, int32_t* peers) {
 
 int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein) {
   std::vector<int> rad;
-  int L = 0;
+  int L = 0, variant = 0;
   bool blue = false;
   if (n < 1) return fail(SHT_ERR_CONFIG, "ring length must be >= 1");
-  if (fft_choose(n, rad, L, blue)) return fail(SHT_ERR_CONFIG, "no FFT plan for this length");
+  if (fft_choose(n, variant, rad, L, blue)) return fail(SHT_ERR_CONFIG, "no FFT plan for this length");
   if (radices)
     for (size_t k = 0; k < rad.size() && k < 32; ++k) radices[k] = rad[k];
   if (nstages) *nstages = (int32_t)rad.size();
@@ -742,7 +744,8 @@ int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
     if (int rc = alltoall(p, true, s)) return rc;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][2], s));
   const FftParams fp = fft_params(p);
-  for (int c : {1, 2, 0}) launch_fft(false, c, fp, p->fft_w0[c], p->fft_nw[c], p->Y, grid, p->fft_smem[c], s);
+  for (int c = 1; c < kFftVariants; ++c)
+    launch_fft(false, c, fp, p->fft_w0[c], p->fft_nw[c], p->Y, grid, p->fft_smem[c], s);
   SHT_CUDA_TRY(cudaGetLastError());
   if (prof) {
     SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][3], s));
@@ -759,7 +762,8 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][4], s));
   const FftParams fp = fft_params(p);
-  for (int c : {1, 2, 0}) launch_fft(true, c, fp, p->fft_w0[c], p->fft_nw[c], grid, p->Y, p->fft_smem[c], s);
+  for (int c = 1; c < kFftVariants; ++c)
+    launch_fft(true, c, fp, p->fft_w0[c], p->fft_nw[c], grid, p->Y, p->fft_smem[c], s);
   SHT_CUDA_TRY(cudaGetLastError());
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][5], s));
   if (p->nranks > 1)
@@ -783,7 +787,7 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
 int sht_kernel_launches(const sht_plan* p, int* per_pair) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   int fft = 0;
-  for (int c = 0; c < 3; ++c) fft += p->fft_nw[c] > 0;
+  for (int c = 1; c < kFftVariants; ++c) fft += p->fft_nw[c] > 0;
   if (per_pair) *per_pair = (p->ntiles_inv > 0) + (p->ntiles_dir > 0) + 2 * fft;
   return SHT_OK;
 }
