@@ -109,6 +109,11 @@ const char* sht_last_error(void);
 
 /* ---- host-only helpers (no GPU needed; used by the CPU test-suite) ---- */
 
+/* Build every rank's plan tables on the host without touching the GPU
+ * (layouts, partition, FFT plans, shared-memory fits); SHT_OK if
+ * sht_plan_create would accept these arguments. */
+int sht_plan_validate(int truncation, int ndgl, const int32_t* nloen, int nfld, int nranks);
+
 /* Gaussian nodes of the northern hemisphere, pole -> equator (ndgl/2 each):
  * mu = sin(latitude), sint = cos(latitude), w = Gaussian weight. */
 int sht_gauss_nodes(int ndgl, double* mu, double* sint, double* w);

@@ -7,7 +7,7 @@ an NCCL all-to-all for the grid <-> spectral transposition across GPUs.
 """
 
 from .errors import ConfigurationError, ProtocolError, SHTError
-from .transform import SHTransform, alltoall_order, alltoall_rows, fft_plan_info, gauss_nodes, nspec_real, octahedral_nloen, partition
+from .transform import SHTransform, alltoall_order, alltoall_rows, fft_plan_info, plan_validate, gauss_nodes, nspec_real, octahedral_nloen, partition
 
 __all__ = [
     "SHTransform",
@@ -21,4 +21,5 @@ __all__ = [
     "fft_plan_info",
     "alltoall_rows",
     "alltoall_order",
+    "plan_validate",
 ]

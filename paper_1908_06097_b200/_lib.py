@@ -26,7 +26,7 @@ SHT_FLAG_PROFILE_PHASES = 2
 EXPORTS = (
     "sht_version", "sht_plan_create", "sht_inv_trans", "sht_dir_trans", "sht_local_layout",
     "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
-    "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
+    "sht_plan_validate", "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
 )
 
 _lib = None
@@ -62,6 +62,7 @@ def load() -> C.CDLL:
     lib.sht_nccl_get_unique_id.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.restype = None
+    lib.sht_plan_validate.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int]
     lib.sht_gauss_nodes.argtypes = [C.c_int, f64p, f64p, f64p]
     lib.sht_partition.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i32p, i32p]
     lib.sht_alltoall_rows.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i64p]

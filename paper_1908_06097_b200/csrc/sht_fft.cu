@@ -50,6 +50,10 @@ __device__ __forceinline__ double2 mul_pi(double2 a) { return make_double2(-a.y,
 
 __device__ __forceinline__ int fdiv(int x, uint64_t mag) { return (int)(((uint64_t)(unsigned)x * mag) >> 40); }
 
+// Padded shared-memory slot of FFT point x: one spare slot per 16 points, so
+// the contiguous pencils of the last step (stride R) spread over the banks.
+__device__ __forceinline__ int px(int x) { return x + (x >> 4); }
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -84,16 +88,13 @@ __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, in
     const int pp = b - q * np;
     const int blk = fdiv(pp, st.mag_S);
     const int s = pp - blk * S;
-    double2* base = buf + q * L + blk * st.B + s;
+    const int i0 = q * L + blk * st.B + s;
     double2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = base[r * S];
+    for (int r = 0; r < R; ++r) v[r] = buf[px(i0 + r * S)];
     double2 w1 = make_double2(1.0, 0.0);
     const bool twd = tw && s > 0;
-    if (twd) {
-      const int e = s * st.tmul;
-      w1 = cmul(tw2[kTwLo + (e >> 6)], tw2[e & (kTwLo - 1)]);
-    }
+    if (twd) w1 = cmul(tw2[st.tw_hi + (s >> 5)], tw2[st.tw_lo + (s & 31)]);
     if (!kFwd && twd) {
       double2 wr = w1;
       v[1] = cmul(v[1], w1);
@@ -116,10 +117,10 @@ __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, in
     if (kPost) {  // last DIT step: S == 1, positions blk * R + r
       const double2* bh = bhat + blk * R;
 #pragma unroll
-      for (int r = 0; r < R; ++r) base[r] = conjc(cmul(v[r], __ldg(bh + r)));
+      for (int r = 0; r < R; ++r) buf[px(i0 + r)] = conjc(cmul(v[r], __ldg(bh + r)));
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) base[r * S] = v[r];
+      for (int r = 0; r < R; ++r) buf[px(i0 + r * S)] = v[r];
     }
   }
   __syncthreads();
@@ -180,7 +181,7 @@ struct RingSmem {
   FftRing rg;
   FftWork wk;
   FftStep st[kMaxSteps];
-  double2 tw[kTwLo + kTwHi];
+  double2 tw[kTwMax];
 };
 
 __device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, int w) {
@@ -190,8 +191,7 @@ __device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, int 
   }
   __syncthreads();
   if ((int)threadIdx.x < rs.rg.nstep) rs.st[threadIdx.x] = p.steps[rs.rg.step0 + threadIdx.x];
-  const int ntw = kTwLo + (rs.rg.L + kTwLo - 1) / kTwLo;
-  for (int t = threadIdx.x; t < ntw; t += blockDim.x) rs.tw[t] = p.tw[rs.rg.tw2_off + t];
+  for (int t = threadIdx.x; t < rs.rg.ntw; t += blockDim.x) rs.tw[t] = p.tw[rs.rg.tw2_off + t];
   __syncthreads();
 }
 
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   const FftRing& rg = rs.rg;
   const int N = rg.n, L = rg.L, M = rg.mcap;
   double2* buf = smc;
-  double2* stg = smc + (size_t)rg.nb * L;  // nb == 1: northern F^a, F^b of the current pair, [m][2]
+  double2* stg = smc + fft_slots((size_t)rg.nb * L);  // nb == 1: northern F^a, F^b of the current pair
   const bool blue = rg.chirp_off >= 0;
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
       const int fa = 2 * (bt.pa + (bt.side < 0 ? (q >> 1) : 0));
       const int side = bt.side < 0 ? (q & 1) : bt.side;
-      double* dst = reinterpret_cast<double*>(buf + idx);
-      if (n < N) {
+      double* dst = reinterpret_cast<double*>(buf + px(idx));
+      if (n < N && !(p.debug & 2)) {
         const int64_t go = (side ? rg.goff_s : rg.goff_n) + n;
         cp_async8(dst, grid + (int64_t)fa * p.grid_ld + go);
         if (fa + 1 < p.nfld)
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
         else
           dst[1] = 0.0;
       } else {
-        buf[idx] = make_double2(0.0, 0.0);
+        buf[px(idx)] = make_double2(0.0, 0.0);
       }
     }
     cp_async_commit();
@@ -263,14 +263,14 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     if (blue) {
       for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
         const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
-        if (n < N) buf[idx] = cmul(buf[idx], __ldg(chirp + n));
+        if (n < N) buf[px(idx)] = cmul(buf[px(idx)], __ldg(chirp + n));
       }
       __syncthreads();
     }
     if (!(p.debug & 1)) ring_dft<V>(buf, L, bt.nseq, rs.st, rg.nstep, rs.tw, blue, bhat);
     auto Z = [&](int q, int k) {
-      if (blue) return cmul(__ldg(chirp + k), conjc(buf[q * L + k]));
-      return buf[q * L + dit_pos(k, rs.st, rg.nstep)];
+      if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]));
+      return buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
     };
     auto split = [&](int q, int m, double2& fa, double2& fb) {
       const double2 zm = Z(q, m), zn = Z(q, m == 0 ? 0 : N - m);
@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
         const int fa = 2 * (bt.pa + pl);
         const int64_t row = p.yrow[rg.yrow_off + m];
         double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
+        if (p.debug & 4) continue;
         __stcs(d, make_double2(w * (na.x + sa.x), w * (na.y + sa.y)));
         __stcs(d + 1, make_double2(w * (na.x - sa.x), w * (na.y - sa.y)));
         if (fa + 1 < p.nfld) {
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
           const double2 na = stg[2 * m], nbv = stg[2 * m + 1];
           const int64_t row = p.yrow[rg.yrow_off + m];
           double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
+          if (p.debug & 4) continue;
           __stcs(d, make_double2(w * (na.x + xa.x), w * (na.y + xa.y)));
           __stcs(d + 1, make_double2(w * (na.x - xa.x), w * (na.y - xa.y)));
           if (fa + 1 < p.nfld) {
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     for (int idx = threadIdx.x; idx < bt.nseq * gap; idx += NT) {
       const int q = idx / gap, g = idx - q * gap;
       const int k = g < N - 2 * M - 1 ? M + 1 + g : N + (g - (N - 2 * M - 1));
-      buf[q * L + k] = make_double2(0.0, 0.0);
+      buf[px(q * L + k)] = make_double2(0.0, 0.0);
     }
     // Fourier rows -> conj(Z) of both hemispheres at k = m and k = N - m
     // (one thread per (m, field pair): a row's 64-byte chunks are read once)
@@ -351,9 +353,12 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       const int fa = 2 * (bt.pa + pl);
       const int64_t row = p.yrow[rg.yrow_off + m];
       const double2* src = reinterpret_cast<const double2*>(four + row * rowd + (int64_t)fa * 4);
-      const double2 sa = __ldcs(src), aa = __ldcs(src + 1);
-      double2 sb = make_double2(0.0, 0.0), ab = sb;
-      if (fa + 1 < p.nfld) {
+      double2 sa = make_double2(0.0, 0.0), aa = sa, sb = sa, ab = sa;
+      if (!(p.debug & 2)) {
+        sa = __ldcs(src);
+        aa = __ldcs(src + 1);
+      }
+      if (fa + 1 < p.nfld && !(p.debug & 2)) {
         sb = __ldcs(src + 2);
         ab = __ldcs(src + 3);
       }
@@ -373,8 +378,8 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
           lo = cmul(lo, __ldg(chirp + m));
           if (m) hi = cmul(hi, __ldg(chirp + N - m));
         }
-        buf[q * L + m] = lo;
-        if (m) buf[q * L + N - m] = hi;
+        buf[px(q * L + m)] = lo;
+        if (m) buf[px(q * L + N - m)] = hi;
       }
     }
     __syncthreads();
@@ -383,10 +388,11 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
       const int pl = bt.side >= 0 ? 0 : (q >> 1);
       const int side = bt.side >= 0 ? bt.side : (q & 1);
-      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[q * L + k]))
-                             : buf[q * L + dit_pos(k, rs.st, rg.nstep)];
+      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]))
+                             : buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
       const int fa = 2 * (bt.pa + pl);
       const int64_t go = (side ? rg.goff_s : rg.goff_n) + k;
+      if (p.debug & 4) continue;
       __stcs(grid + (int64_t)fa * p.grid_ld + go, r.x);
       if (fa + 1 < p.nfld) __stcs(grid + (int64_t)(fa + 1) * p.grid_ld + go, -r.y);
     }
@@ -411,7 +417,7 @@ static void launch_one(bool g2f, const FftParams& p, int w0, int nw, const doubl
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s) {
   if (nw <= 0) return;
-  if (variant == 1) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
+  if (variant == 1 || variant == 3) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
   if (variant == 2) launch_one<2>(g2f, p, w0, nw, in, out, smem, s);
 }
 
@@ -487,30 +493,35 @@ int fft_pos(int k, const std::vector<int>& radices) {
 }
 
 void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
-               int64_t& tw2_off) {
+               int64_t& tw2_off, int& ntw) {
   const long double two_pi = 6.283185307179586476925286766559005768L;
+  tw2_off = (int64_t)arena.size();
   int B = L;
-  for (int R : radices) {
+  for (size_t j = 0; j < radices.size(); ++j) {
+    const int R = radices[j];
     FftStep st;
     st.R = R;
     st.B = B;
     st.S = B / R;
     st.np = L / R;
-    st.tmul = L / B;
-    st.pad = 0;
     st.mag_S = ((uint64_t)1 << 40) / (uint64_t)st.S + 1;
     st.mag_np = ((uint64_t)1 << 40) / (uint64_t)st.np + 1;
     st.mag_R = ((uint64_t)1 << 40) / (uint64_t)R + 1;
+    st.tw_lo = st.tw_hi = 0;
+    if (j + 1 < radices.size()) {  // W_B^s = hi[s / 32] lo[s % 32], s < S
+      auto W = [&](long long e) {
+        const long double a = -two_pi * (long double)(e % B) / (long double)B;
+        return make_double2((double)cosl(a), (double)sinl(a));
+      };
+      st.tw_lo = (int)(arena.size() - tw2_off);
+      for (int e = 0; e < 32; ++e) arena.push_back(W(e));
+      st.tw_hi = (int)(arena.size() - tw2_off);
+      for (int h = 0; h < (st.S + 31) / 32; ++h) arena.push_back(W(32LL * h));
+    }
     out.push_back(st);
     B = st.S;
   }
-  tw2_off = (int64_t)arena.size();
-  auto W = [&](long long e) {
-    const long double a = -two_pi * (long double)(e % L) / (long double)L;
-    return make_double2((double)cosl(a), (double)sinl(a));
-  };
-  for (int e = 0; e < kTwLo; ++e) arena.push_back(W(e));
-  for (int h = 0; h < (L + kTwLo - 1) / kTwLo; ++h) arena.push_back(W((long long)h * kTwLo));
+  ntw = (int)(arena.size() - tw2_off);
 }
 
 }  // namespace sht

@@ -67,8 +67,7 @@ size_t leg_dir_smem();
 // ---------------------------------------------------------------- ring FFTs
 constexpr int kMaxSteps = 4;
 constexpr int kFftMaxLen = 6912;                   // longest transform one CTA handles
-constexpr int kTwLo = 64;                          // two-level twiddle table: W_L^e = hi[e / 64] lo[e % 64]
-constexpr int kTwHi = (kFftMaxLen + kTwLo - 1) / kTwLo;
+constexpr int kTwMax = 320;                        // per-ring step-twiddle table entries (shared memory)
 
 // One step of the in-place "pencil" FFT of length L = R_0 R_1 ... R_{d-1}:
 // blocks of length B = R_j S, each holding S pencils of R points at stride S.
@@ -77,8 +76,8 @@ struct FftStep {
   int32_t S;           // pencil stride = B / R
   int32_t B;           // block length
   int32_t np;          // pencils per sequence = L / R
-  int32_t tmul;        // L / B: twiddle W_B^(r s) = W_L^(r s tmul)
-  int32_t pad;
+  int32_t tw_lo;       // step twiddles W_B^s = hi[s / 32] lo[s % 32]: offsets in the ring's table
+  int32_t tw_hi;
   uint64_t mag_S, mag_np, mag_R;  // multiply-shift (>> 40) divisors
 };
 
@@ -97,7 +96,9 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   int64_t goff_n;      // offset of the northern ring in the local grid field
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
-  int64_t tw2_off;     // arena offset of lo[0..63] = W_L^e, then hi[h] = W_L^(64 h), h < ceil(L/64)
+  int64_t tw2_off;     // arena offset of this ring's step-twiddle table (ntw entries)
+  int32_t ntw;
+  int32_t pad2;
   double w;            // Gaussian weight
 };
 
@@ -119,16 +120,19 @@ struct FftParams {
   int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT steps
 };
 
-// Ring-FFT kernel variants: 1 = pencils <= 16 points, 256 threads, 2 CTAs/SM;
-// 2 = pencils up to 31 points (primes 17..31), 256 threads, 1 CTA/SM.
-constexpr int kFftVariants = 3;  // index 0 unused
+// Ring-FFT launch classes: 1 = pencils <= 16 points, 256 threads, <= 104 KB
+// (2 CTAs/SM); 2 = pencils up to 31 points (primes 17..31), 1 CTA/SM;
+// 3 = class-1 kernel with up to 216 KB of shared memory (1 CTA/SM).
+constexpr int kFftVariants = 4;  // index 0 unused
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s);
 // Plan for a ring of n points: kernel variant, pencil radices and transform
 // length (n, or a 13-smooth Bluestein length L >= 2n-1).
 int fft_choose(int n, int& variant, std::vector<int>& radices, int& L, bool& bluestein);
 void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
-               int64_t& tw2_off);
+               int64_t& tw2_off, int& ntw);
+// Shared-memory complex slots for n FFT points (one pad slot per 16 against bank conflicts).
+__host__ __device__ inline size_t fft_slots(size_t n) { return n + n / 16 + 1; }
 // Position of DFT output k after the in-place DIT pencil FFT (digit reversal).
 int fft_pos(int k, const std::vector<int>& radices);
 

@@ -239,7 +239,7 @@ static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, 
   return SHT_OK;
 }
 
-static int build_plan(sht_plan* p, const void* nccl_id) {
+static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   const Geometry& g = p->g;
   const int T = g.T, nh = g.nh, P = p->nranks, r = p->rank, nfld = p->nfld;
   gauss_nodes_ld(g.ndgl, p->mu, p->sint, p->w);
@@ -356,7 +356,7 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   p->grid_ld = go;
   const int npairs = (nfld + 1) / 2;
   // shared memory per CTA: variant 1 runs 2 CTAs/SM, variant 2 one
-  const size_t budget[kFftVariants] = {0, 108 * 1024, 216 * 1024};
+  const size_t budget[kFftVariants] = {0, 104 * 1024, 216 * 1024, 216 * 1024};
   std::vector<FftStep> steps;
   std::vector<int64_t> ring_cost(nlr, 0);
   int64_t nfour_local = 0;
@@ -379,7 +379,8 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
     R.nstep = (int)rad.size();
     R.step0 = (int)steps.size();
-    fft_steps(L, rad, steps, arena, R.tw2_off);
+    fft_steps(L, rad, steps, arena, R.tw2_off, R.ntw);
+    if (R.ntw > kTwMax) return fail(SHT_ERR_CONFIG, "step-twiddle table too large (N=" + std::to_string(R.n) + ")");
     const long double pi_ld = 3.14159265358979323846264338327950288L;
     R.chirp_off = R.bhat_off = -1;
     if (blue) {
@@ -420,13 +421,21 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
     // they fit, else one sequence at a time (nb = 1; g2f stages the northern
     // coefficients, (M+1) x 2 complex)
     auto smem = [&](int nb) {
-      return ((size_t)nb * L + (nb == 1 ? 2 * (size_t)(R.mcap + 1) : 0)) * sizeof(double2);
+      return (fft_slots((size_t)nb * L) + (nb == 1 ? 2 * (size_t)(R.mcap + 1) : 0)) * sizeof(double2);
     };
     int K = std::min(npairs, 64), nb = 2 * K;
     while (K > 1 && smem(2 * K) > budget[variant]) nb = 2 * --K;
     if (smem(nb) > budget[variant]) nb = 1;
+    if (smem(nb) > budget[variant] && variant == 1) {  // one CTA per SM with more shared memory
+      variant = 3;
+      K = std::min(npairs, 64);
+      nb = 2 * K;
+      while (K > 1 && smem(2 * K) > budget[variant]) nb = 2 * --K;
+      if (smem(nb) > budget[variant]) nb = 1;
+    }
     if (smem(nb) > budget[variant])
       return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+    R.variant = variant;
     R.K = K;
     R.nb = nb;
     p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb));
@@ -469,6 +478,8 @@ static int build_plan(sht_plan* p, const void* nccl_id) {
   for (int d = 0; d < P; ++d)
     if (d != r) sent += p->xrows[d];
   p->work_a2a = 2.0 * (double)sent * nfld * 32.0;
+
+  if (dry_run) return SHT_OK;
 
   // ---- device side
   int dev = 0;
@@ -616,6 +627,22 @@ int sht_gauss_nodes(int ndgl, double* mu, double* sint, double* w) {
   if (mu) std::copy(a.begin(), a.end(), mu);
   if (sint) std::copy(b.begin(), b.end(), sint);
   if (w) std::copy(c.begin(), c.end(), w);
+  return SHT_OK;
+}
+
+int sht_plan_validate(int truncation, int ndgl, const int32_t* nloen, int nfld, int nranks) {
+  if (nfld < 1) return fail(SHT_ERR_CONFIG, "nfld must be >= 1");
+  if (nranks < 1) return fail(SHT_ERR_CONFIG, "invalid nranks");
+  for (int r = 0; r < nranks; ++r) {
+    sht_plan* p = new sht_plan();
+    p->nfld = nfld;
+    p->rank = r;
+    p->nranks = nranks;
+    int rc = make_geometry(truncation, ndgl, nloen, p->g);
+    if (!rc) rc = build_plan(p, nullptr, true);
+    delete p;
+    if (rc) return rc;
+  }
   return SHT_OK;
 }
 

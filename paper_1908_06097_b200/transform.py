@@ -251,6 +251,13 @@ def _nloen_arg(truncation: int, grid):
     return arr.ctypes.data_as(_lib.i32p), int(arr.size), arr
 
 
+def plan_validate(truncation: int, nfld: int, nranks: int = 1, grid="octahedral") -> None:
+    """Build every rank's plan tables on the host (no GPU); raise ConfigurationError if unsupported."""
+    lib = _lib.load()
+    ptr, ndgl, _keep = _nloen_arg(truncation, grid)
+    _lib.check(lib.sht_plan_validate(int(truncation), ndgl, ptr, int(nfld), int(nranks)))
+
+
 def alltoall_rows(truncation: int, nranks: int, grid="octahedral") -> np.ndarray:
     """[P, P] Fourier rows rank r sends to rank d in the inverse transposition (host-only call).
 

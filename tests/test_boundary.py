@@ -133,3 +133,21 @@ def test_errors_map_to_reference_classes(lib):
         partition(10, 2, grid=np.array([20, 24, 28, 20]))     # not symmetric
     with pytest.raises(ConfigurationError):
         alltoall_order(2, 5)
+
+
+@pytest.mark.parametrize("T,nfld,P", [(79, 10, 1), (639, 548, 1), (639, 548, 2), (639, 548, 4), (639, 548, 8),
+                                      (639, 7, 3), (319, 65, 4), (15, 1, 2)])
+def test_plan_validate_host_only(lib, T, nfld, P):
+    """Every rank's plan (layouts, FFT plans, shared-memory fits) builds on the host."""
+    from paper_1908_06097_b200 import plan_validate
+
+    plan_validate(T, nfld, P)
+
+
+def test_plan_validate_rejects_unsupported(lib):
+    from paper_1908_06097_b200 import ConfigurationError, plan_validate
+
+    with pytest.raises(ConfigurationError):
+        plan_validate(1279, 548, 8)          # equator rings > 6912-point Bluestein: not built yet
+    with pytest.raises(ConfigurationError):
+        plan_validate(79, 0, 1)
