@@ -7,9 +7,11 @@
 // GEMMs are built from warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4),
 // the only FP64 tensor path on B200; measured issue peak 37.1 TFLOP/s at
 // 1965 MHz (profiles/r01_probe_fp64.json).  Operands are staged HBM -> shared
-// memory with a 3-stage cp.async (LDGSTS, zero-fill for ragged edges) pipeline;
-// fragments are read with conflict-free 128-bit LDS; a persistent CTA per SM
-// pulls tiles (largest K first) from an atomic ticket.
+// memory by 1-D bulk copies (TMA, cp.async.bulk -> SASS UBLKCP) completing on
+// per-stage mbarriers (2 stages of 64 wavenumbers / 32 rings); fragments are
+// read with 128-bit LDS; a persistent CTA per SM pulls tiles (m ascending,
+// largest K first) from an atomic ticket and prefetches the next tile's
+// operands under the current tile's epilogue.
 //
 // Parity split (SURVEY.md App. A "Hemispheric split"): for each m the S
 // accumulator takes the even n-m and the A accumulator the odd n-m.  Both come
@@ -29,45 +31,75 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+// ---- bulk-copy (TMA 1-D, cp.async.bulk) + mbarrier helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
+constexpr int kLegThreads = 256;
+constexpr int kStages = 2;
 
 // ------------------------------------------------------------------ leg_inv
-constexpr int kInvStages = 2;
 constexpr int kInvPStr = kInvKc + 8;          // 72 doubles: rows of P tile (== 8 mod 16 -> no LDS.128 conflicts)
 constexpr int kInvSStr = 2 * kInvKc + 2;      // 130 doubles: field rows of the spectral tile (== 2 mod 16)
 constexpr int kInvPDbl = kInvRings * kInvPStr;
 constexpr int kInvSDbl = kLegFields * kInvSStr;
 constexpr int kInvStageDbl = kInvPDbl + kInvSDbl;
-constexpr int kLegThreads = 256;
 
 // Tile: rings r0..r0+63 (northern index) x fields f0..f0+63 of wavenumber lm.
 // Warp w: rings 32*(w&1).. , fields 16*(w>>1)..  -> 4 ring groups x 2 field groups
 // x {S.re, S.im, A.re, A.im} DMMA accumulators (64 doubles per thread).
-// Persistent: the next tile's first pipeline stages are issued before the
-// current tile's epilogue stores, so tile switches do not drain the pipeline.
+// Operands arrive by 1-D bulk copies (one per P-table row and per field row,
+// issued by warp 0) completing on a per-stage mbarrier; the next tile's first
+// stages are issued before the current tile's epilogue stores.
 struct InvTile {
-  int lm, r0, f0, K, nk;
+  int lm, r0, f0, K, nk, kp, nrows, nf;
   const double* P;
   const double* S;
-  int kp;
 };
 
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   __shared__ int s_tile;
+  __shared__ __align__(8) uint64_t full[kStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 1, wf = warp >> 1;
   const int lr = lane >> 2, lc = lane & 3;
+
+  // stale operand slots must hold finite values (they meet zero P padding or
+  // feed discarded accumulator rows)
+  for (int i = tid; i < kStages * kInvStageDbl; i += kLegThreads) sm[i] = 0.0;
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  fence_async_smem();
+  __syncthreads();
 
   auto make = [&](int t) {
     InvTile c;
@@ -79,39 +111,35 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     c.kp = p.lm_kp[c.lm];
     c.K = p.T - m + 1;
     c.nk = (c.K + kInvKc - 1) / kInvKc;
+    c.nrows = min(kInvRings, p.nh - c.r0);
+    c.nf = min(kLegFields, p.nfld - c.f0);
     c.P = p.ptab + p.lm_poff[c.lm] + (int64_t)(c.r0 - p.lm_i0[c.lm]) * c.kp;
     c.S = spec + 2 * p.lm_soff[c.lm];
     return c;
   };
-  auto load_stage = [&](const InvTile& c, int kc, int st) {
+  // the bulk copies of k-chunk kc into stage st: one per P row and per field
+  // row, spread over all threads (the tx count may run ahead of expect_tx)
+  auto issue = [&](const InvTile& c, int kc, int st) {
+    if (p.debug & 1) return;
     double* Ps = sm + st * kInvStageDbl;
     double* Ss = Ps + kInvPDbl;
-#pragma unroll
-    for (int it = 0; it < (kInvRings * (kInvKc / 2)) / kLegThreads; ++it) {
-      const int q = tid + it * kLegThreads;
-      const int row = q / (kInvKc / 2), col = q % (kInvKc / 2);
-      const bool v = (c.r0 + row) < p.nh;
-      const double* src = v ? c.P + (int64_t)row * c.kp + kc * kInvKc + col * 2 : p.ptab;
-      cp_async16(Ps + row * kInvPStr + col * 2, src, v);
-    }
-#pragma unroll
-    for (int it = 0; it < (kLegFields * kInvKc) / kLegThreads; ++it) {
-      const int q = tid + it * kLegThreads;
-      const int f = q / kInvKc, n = q % kInvKc;
-      const int kk = kc * kInvKc + n;
-      const bool v = (c.f0 + f) < p.nfld && kk < c.K;
-      const double* src = v ? c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kk : spec;
-      cp_async16(Ss + f * kInvSStr + 2 * n, src, v);
+    const int kcount = min(kInvKc, c.K - kc * kInvKc);
+    if (tid == 0) mbar_expect_tx(&full[st], (unsigned)(c.nrows * kInvKc * 8 + c.nf * kcount * 16));
+    for (int j = tid; j < c.nrows + c.nf; j += kLegThreads) {
+      if (j < c.nrows)
+        bulk_g2s(Ps + j * kInvPStr, c.P + (int64_t)j * c.kp + kc * kInvKc, kInvKc * 8, &full[st]);
+      else {
+        const int f = j - c.nrows;
+        bulk_g2s(Ss + f * kInvSStr, c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kc * kInvKc, kcount * 16,
+                 &full[st]);
+      }
     }
   };
   auto prologue = [&](const InvTile& c) {
-#pragma unroll
-    for (int st = 0; st < kInvStages - 1; ++st) {
-      if (st < c.nk) load_stage(c, st, st);
-      cp_async_commit();
-    }
+    for (int st = 0; st < kStages && st < c.nk; ++st) issue(c, st, st);
   };
 
+  unsigned phase = 0;  // bit st: parity of the next completion of full[st]
   if (tid == 0) s_tile = atomicAdd(p.counter, 1);
   __syncthreads();
   int t = s_tile;
@@ -132,16 +160,12 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
-      cp_async_wait<kInvStages - 2>();
-      __syncthreads();
-      {
-        const int nx = kc + kInvStages - 1;
-        if (nx < c.nk && !(p.debug & 1)) load_stage(c, nx, nx % kInvStages);
-        cp_async_commit();
-      }
+      const int st = kc & 1;
+      if (!(p.debug & 1)) mbar_wait(&full[st], (phase >> st) & 1);
+      phase ^= 1u << st;
       if (active && !(p.debug & 2)) {
-        const double* Ps = sm + (kc % kInvStages) * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
-        const double* Ss = sm + (kc % kInvStages) * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
+        const double* Ps = sm + st * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
+        const double* Ss = sm + st * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
         const int smax = min(kInvKc / 8, (c.K - kc * kInvKc + 7) / 8);
 #pragma unroll
         for (int sub = 0; sub < kInvKc / 8; ++sub) {
@@ -168,15 +192,16 @@ __global__ void __launch_bounds__(kLegThreads, 1)
             }
         }
       }
+      __syncthreads();  // stage st fully consumed
+      if (kc + kStages < c.nk) issue(c, kc + kStages, st);
     }
-    __syncthreads();  // every warp is done with the stage buffers
     if (tid == 0) s_tile = atomicAdd(p.counter, 1);
     __syncthreads();
     const int tn = s_tile;
     InvTile cn;
     if (tn < p.ntiles) {
       cn = make(tn);
-      prologue(cn);  // next tile's loads overlap this tile's stores
+      prologue(cn);  // next tile's operands stream in under this tile's stores
     }
 
     if (active && !(p.debug & 4)) {
@@ -202,33 +227,41 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     }
     if (tn >= p.ntiles) break;
     c = cn;
+    __syncthreads();  // s_tile is rewritten at the end of the next tile
   }
-  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ leg_dir
-constexpr int kDirStages = 2;
 constexpr int kDirPStr = kDirN + 4;            // 132: P tile [ring][n]          (== 4 mod 16)
-constexpr int kDirBStr = 2 * kLegFields + 4;   // 132: S / A tiles [ring][field][re,im]
+constexpr int kDirBStr = 4 * kLegFields + 2;   // 258: B tile [ring][field][S.re, S.im, A.re, A.im]
 constexpr int kDirPDbl = kDirKc * kDirPStr;
 constexpr int kDirBDbl = kDirKc * kDirBStr;
-constexpr int kDirStageDbl = kDirPDbl + 2 * kDirBDbl;
+constexpr int kDirStageDbl = kDirPDbl + kDirBDbl;
 
 // Tile: n-m offsets n0..n0+127 (64 even-parity rows, 64 odd) x fields f0..f0+63.
 // Warp w: n 64*(w&1).. (4 groups of 8 (S,A) row pairs), fields 16*(w>>1)..
 struct DirTile {
-  int lm, n0, f0, K, i0, nrings, nk, kp;
+  int lm, n0, f0, K, i0, nrings, nk, kp, nf;
   const double* P;
 };
 
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_dir_kernel(const LegParams p, const double* __restrict__ four, double* __restrict__ spec) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   __shared__ int s_tile;
+  __shared__ __align__(8) uint64_t full[kStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wn = warp & 1, wf = warp >> 1;
   const int lr = lane >> 2, lc = lane & 3;
   const int64_t rowd = (int64_t)p.nfld * 4;
+
+  for (int i = tid; i < kStages * kDirStageDbl; i += kLegThreads) sm[i] = 0.0;
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  fence_async_smem();
+  __syncthreads();
 
   auto make = [&](int t) {
     DirTile c;
@@ -242,43 +275,39 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     c.K = p.T - m + 1;
     c.nrings = p.nh - c.i0;
     c.nk = (c.nrings + kDirKc - 1) / kDirKc;
+    c.nf = min(kLegFields, p.nfld - c.f0);
     c.P = p.ptab + p.lm_poff[c.lm];
     return c;
   };
-  auto load_stage = [&](const DirTile& c, int kc, int st) {
+  auto issue = [&](const DirTile& c, int kc, int st) {
+    if (p.debug & 1) return;
     double* Ps = sm + st * kDirStageDbl;
-    double* Ss = Ps + kDirPDbl;
-    double* As = Ss + kDirBDbl;
-#pragma unroll
-    for (int it = 0; it < (kDirKc * (kDirN / 2)) / kLegThreads; ++it) {
-      const int q = tid + it * kLegThreads;
-      const int rr = q >> 6, cc = q & 63;
-      const int ring = kc * kDirKc + rr;  // relative to i0
-      const int nn = c.n0 + 2 * cc;
-      const bool v = ring < c.nrings && nn < c.K;
-      const double* src = v ? c.P + (int64_t)ring * c.kp + nn : p.ptab;
-      cp_async16(Ps + rr * kDirPStr + 2 * cc, src, v);
+    double* Bs = Ps + kDirPDbl;
+    const int nr = min(kDirKc, c.nrings - kc * kDirKc);
+    const int pbytes = min(kDirN, c.kp - c.n0) * 8;
+    if (warp == 0) {
+      // rings past the end inside the last 4-ring k-step must contribute zero;
+      // the arrive (release) follows the zero stores
+      for (int rr = nr; rr < ((nr + 3) & ~3); ++rr)
+        for (int q = lane; q < kDirN; q += 32) Ps[rr * kDirPStr + q] = 0.0;
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(&full[st], (unsigned)(nr * (pbytes + c.nf * 32)));
     }
-#pragma unroll
-    for (int it = 0; it < (kDirKc * kLegFields * 2) / kLegThreads; ++it) {
-      const int q = tid + it * kLegThreads;
-      const int rr = q >> 7, rem = q & 127;
-      const int f = rem >> 1, half = rem & 1;
-      const int ring = kc * kDirKc + rr;
-      const bool v = ring < c.nrings && (c.f0 + f) < p.nfld;
-      const double* src =
-          v ? four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd + (int64_t)(c.f0 + f) * 4 + 2 * half : four;
-      cp_async16((half ? As : Ss) + rr * kDirBStr + 2 * f, src, v);
+    for (int j = tid; j < 2 * nr; j += kLegThreads) {
+      const int rr = j >> 1;
+      const int ring = kc * kDirKc + rr;  // relative to i0
+      if (j & 1)
+        bulk_g2s(Bs + rr * kDirBStr, four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd + (int64_t)c.f0 * 4,
+                 c.nf * 32, &full[st]);
+      else
+        bulk_g2s(Ps + rr * kDirPStr, c.P + (int64_t)ring * c.kp + c.n0, pbytes, &full[st]);
     }
   };
   auto prologue = [&](const DirTile& c) {
-#pragma unroll
-    for (int st = 0; st < kDirStages - 1; ++st) {
-      if (st < c.nk) load_stage(c, st, st);
-      cp_async_commit();
-    }
+    for (int st = 0; st < kStages && st < c.nk; ++st) issue(c, st, st);
   };
 
+  unsigned phase = 0;
   if (tid == 0) s_tile = atomicAdd(p.counter, 1);
   __syncthreads();
   int t = s_tile;
@@ -299,17 +328,12 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
-      cp_async_wait<kDirStages - 2>();
-      __syncthreads();
-      {
-        const int nx = kc + kDirStages - 1;
-        if (nx < c.nk && !(p.debug & 1)) load_stage(c, nx, nx % kDirStages);
-        cp_async_commit();
-      }
+      const int st = kc & 1;
+      if (!(p.debug & 1)) mbar_wait(&full[st], (phase >> st) & 1);
+      phase ^= 1u << st;
       if (active && !(p.debug & 2)) {
-        const double* Ps = sm + (kc % kDirStages) * kDirStageDbl + lc * kDirPStr + wn * 64 + 2 * lr;
-        const double* Ss = sm + (kc % kDirStages) * kDirStageDbl + kDirPDbl + lc * kDirBStr + 2 * (wf * 16 + lr);
-        const double* As = Ss + kDirBDbl;
+        const double* Ps = sm + st * kDirStageDbl + lc * kDirPStr + wn * 64 + 2 * lr;
+        const double* Bs = sm + st * kDirStageDbl + kDirPDbl + lc * kDirBStr + 4 * (wf * 16 + lr);
         const int kmax = min(kDirKc / 4, (c.nrings - kc * kDirKc + 3) / 4);
 #pragma unroll
         for (int ks = 0; ks < kDirKc / 4; ++ks) {
@@ -320,8 +344,9 @@ __global__ void __launch_bounds__(kLegThreads, 1)
             a[g] = *reinterpret_cast<const double2*>(Ps + ks * 4 * kDirPStr + 16 * g);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            bs[h] = *reinterpret_cast<const double2*>(Ss + ks * 4 * kDirBStr + 16 * h);
-            ba[h] = *reinterpret_cast<const double2*>(As + ks * 4 * kDirBStr + 16 * h);
+            const double* bp = Bs + ks * 4 * kDirBStr + 32 * h;
+            bs[h] = *reinterpret_cast<const double2*>(bp);
+            ba[h] = *reinterpret_cast<const double2*>(bp + 2);
           }
 #pragma unroll
           for (int g = 0; g < 4; ++g)
@@ -336,8 +361,9 @@ __global__ void __launch_bounds__(kLegThreads, 1)
             }
         }
       }
+      __syncthreads();
+      if (kc + kStages < c.nk) issue(c, kc + kStages, st);
     }
-    __syncthreads();
     if (tid == 0) s_tile = atomicAdd(p.counter, 1);
     __syncthreads();
     const int tn = s_tile;
@@ -369,8 +395,8 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     }
     if (tn >= p.ntiles) break;
     c = cn;
+    __syncthreads();
   }
-  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ leg_poly
@@ -452,8 +478,8 @@ __global__ void leg_poly_kernel(int T, int nh, const int32_t* __restrict__ lm_m,
 
 }  // namespace
 
-size_t leg_inv_smem() { return (size_t)kInvStages * kInvStageDbl * sizeof(double); }
-size_t leg_dir_smem() { return (size_t)kDirStages * kDirStageDbl * sizeof(double); }
+size_t leg_inv_smem() { return (size_t)kStages * kInvStageDbl * sizeof(double); }
+size_t leg_dir_smem() { return (size_t)kStages * kDirStageDbl * sizeof(double); }
 
 void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s) {
   static bool attr = false;
