@@ -15,11 +15,14 @@
 // and writes them back to the same addresses.  No value crosses a barrier in
 // registers and no second buffer is needed, so a 2576-point ring pair for one
 // field pair needs 82 KB and two CTAs share an SM.  The decimation-in-time
-// order leaves the spectrum digit-reversed; the transposed algorithm (steps in
-// reverse order, twiddles before the codelet) maps digit-reversed input back
-// to natural order.  Rings with a prime factor > 31 use Bluestein's algorithm
-// with a 13-smooth L >= 2N-1: DIT FFT, product with the kernel spectrum
-// (stored digit-reversed, fused into the last step), reverse FFT.
+// order leaves the spectrum digit-reversed (extraction reads it through
+// dit_pos).  A prime factor p > 31 of N becomes a Bluestein step (factor-local
+// chirp-z): its DFT_p pencils are gathered G at a time into a work buffer,
+// convolved with the chirp kernel by an inner pencil FFT of 13-smooth length
+// Lp >= 2p-1 (DIT, kernel product fused into the last inner step, then the
+// transposed steps that map digit-reversed back to natural order) and
+// scattered back; the ring itself is never padded, so rings up to 8192 points
+// (TCo1999) fit one CTA.
 //
 // Fusions: g2f scales by 1/N and combines the two hemispheres into the
 // parity rows the Legendre GEMM consumes, S' = w_i (F_N + F_S) and
@@ -29,6 +32,7 @@
 // receive/send buffers directly (pack/unpack fused).
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <functional>
 
 #include "sht_internal.h"
@@ -74,12 +78,19 @@ struct FftCfg {
   }
 };
 
+constexpr int kMaxAllSteps = 3 * kMaxSteps;  // ring steps + inner steps of up to two Bluestein steps
+
+// W^e of a transform from its 2-level table at `base` (lo[64], hi[...]).
+__device__ __forceinline__ double2 tw_at(const double2* __restrict__ twt, int base, int e) {
+  return cmul(twt[base + 64 + (e >> 6)], twt[base + (e & 63)]);
+}
+
 // One pencil step over nseq sequences of length L (in place).  kFwd: DIT
 // step (codelet, then twiddle); else transposed step (twiddle, then codelet).
-// kPost: last DIT step of Bluestein's first FFT: store conj(X * bhat).
+// kPost: last DIT step of a Bluestein convolution: store conj(X * bhat).
 template <int R, int V, bool kFwd, bool kPost>
 __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, int L, const FftStep& st, bool tw,
-                                         const double2* __restrict__ tw2, const double2* __restrict__ bhat) {
+                                         const double2* __restrict__ twt, const double2* __restrict__ bhat) {
   constexpr int NT = FftCfg<V>::kThreads;
   const int np = st.np, S = st.S;
   const int total = nseq * np;
@@ -92,9 +103,9 @@ __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, in
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = buf[px(i0 + r * S)];
-    double2 w1 = make_double2(1.0, 0.0);
     const bool twd = tw && s > 0;
-    if (twd) w1 = cmul(tw2[st.tw_hi + (s >> 5)], tw2[st.tw_lo + (s & 31)]);
+    double2 w1 = make_double2(1.0, 0.0);
+    if (twd) w1 = tw_at(twt, st.tw_base, s * st.tmul);
     if (!kFwd && twd) {
       double2 wr = w1;
       v[1] = cmul(v[1], w1);
@@ -128,11 +139,11 @@ __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, in
 
 template <int V, bool kFwd, bool kPost>
 __device__ __forceinline__ void step_dispatch(double2* buf, int nseq, int L, const FftStep& st, bool tw,
-                                              const double2* __restrict__ tw2, const double2* __restrict__ bhat) {
+                                              const double2* __restrict__ twt, const double2* __restrict__ bhat) {
   switch (st.R) {
 #define SHT_CASE(R)                                                                                  \
   case R:                                                                                            \
-    if constexpr (FftCfg<V>::template has<R>()) step_run<R, V, kFwd, kPost>(buf, nseq, L, st, tw, tw2, bhat); \
+    if constexpr (FftCfg<V>::template has<R>()) step_run<R, V, kFwd, kPost>(buf, nseq, L, st, tw, twt, bhat); \
     break;
     SHT_CASE(2) SHT_CASE(3) SHT_CASE(4) SHT_CASE(5) SHT_CASE(6) SHT_CASE(7) SHT_CASE(8) SHT_CASE(9)
     SHT_CASE(10) SHT_CASE(11) SHT_CASE(12) SHT_CASE(13) SHT_CASE(14) SHT_CASE(15) SHT_CASE(16)
@@ -145,21 +156,78 @@ __device__ __forceinline__ void step_dispatch(double2* buf, int nseq, int L, con
   }
 }
 
-// The ring DFT of nseq sequences in buf (natural order in).  Direct: DIT,
-// spectrum left digit-reversed.  Bluestein: DIT with conj(X bhat) fused into
-// the last step, then the transposed FFT: buf holds conj(conv) in natural order.
+// Bluestein step: every DFT_R pencil (R prime > 31) of the nseq sequences is
+// x -> w_k conj(conv(x w, conj w))_k, the convolution done by the inner pencil
+// FFT of length Lp on G pencils at a time in the work buffer W.
 template <int V>
-__device__ __forceinline__ void ring_dft(double2* buf, int L, int nseq, const FftStep* steps, int nstep,
-                                         const double2* __restrict__ tw2, bool blue,
-                                         const double2* __restrict__ bhat) {
-  for (int j = 0; j < nstep; ++j) {
-    if (blue && j == nstep - 1)
-      step_dispatch<V, true, true>(buf, nseq, L, steps[j], false, tw2, bhat);
-    else
-      step_dispatch<V, true, false>(buf, nseq, L, steps[j], j < nstep - 1, tw2, bhat);
+__device__ void bluestein_step(double2* __restrict__ buf, double2* __restrict__ W, int nseq, int L,
+                               const FftStep& st, bool tw, const FftStep* __restrict__ steps,
+                               const double2* __restrict__ twt, const double2* __restrict__ tab) {
+  constexpr int NT = FftCfg<V>::kThreads;
+  const int R = st.R, S = st.S, Lp = st.Lp;
+  const int total = nseq * st.np;
+  const double2* chirp = tab + st.chirp_off;
+  const double2* bhat = tab + st.bhat_off;
+  for (int g0 = 0; g0 < total; g0 += st.G) {
+    const int ng = min(st.G, total - g0);
+    for (int idx = threadIdx.x; idx < ng * Lp; idx += NT) {
+      const int g = fdiv(idx, st.mag_Lp), r = idx - g * Lp;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < R) {
+        const int pen = g0 + g;
+        const int q = fdiv(pen, st.mag_np), pp = pen - q * st.np;
+        const int blk = fdiv(pp, st.mag_S), s = pp - blk * S;
+        v = cmul(buf[px(q * L + blk * st.B + s + r * S)], __ldg(chirp + r));
+      }
+      W[px(idx)] = v;
+    }
+    __syncthreads();
+    for (int j = 0; j < st.ninner; ++j) {
+      const FftStep& is = steps[st.inner0 + j];
+      if (j == st.ninner - 1)
+        step_dispatch<V, true, true>(W, ng, Lp, is, false, twt, bhat);
+      else
+        step_dispatch<V, true, false>(W, ng, Lp, is, true, twt, bhat);
+    }
+    for (int j = st.ninner - 1; j >= 0; --j)
+      step_dispatch<V, false, false>(W, ng, Lp, steps[st.inner0 + j], j < st.ninner - 1, twt, bhat);
+    for (int idx = threadIdx.x; idx < ng * R; idx += NT) {
+      const int g = fdiv(idx, st.mag_Rb), k = idx - g * R;
+      const int pen = g0 + g;
+      const int q = fdiv(pen, st.mag_np), pp = pen - q * st.np;
+      const int blk = fdiv(pp, st.mag_S), s = pp - blk * S;
+      double2 y = cmul(__ldg(chirp + k), conjc(W[px(g * Lp + k)]));
+      if (tw && s > 0) y = cmul(y, tw_at(twt, st.tw_base, k * s * st.tmul));
+      buf[px(q * L + blk * st.B + s + k * S)] = y;
+    }
+    __syncthreads();
   }
-  if (blue)
-    for (int j = nstep - 1; j >= 0; --j) step_dispatch<V, false, false>(buf, nseq, L, steps[j], j < nstep - 1, tw2, bhat);
+}
+
+// In-place ring DFT of nseq sequences.  Direct / factor-local Bluestein: DIT
+// steps, spectrum left digit-reversed.  Whole-ring Bluestein: chirp-
+// premultiplied input of length L, DIT with conj(X bhat) fused into the last
+// step, then the transposed steps: buf holds conj(conv) in natural order.
+template <int V>
+__device__ __forceinline__ void ring_dft(double2* buf, double2* W, int L, int nseq, const FftStep* steps, int nstep,
+                                         const double2* __restrict__ twt, const double2* __restrict__ tab,
+                                         bool ring_blue, const double2* __restrict__ bhat) {
+  if (ring_blue) {
+    for (int j = 0; j < nstep; ++j) {
+      if (j == nstep - 1)
+        step_dispatch<V, true, true>(buf, nseq, L, steps[j], false, twt, bhat);
+      else
+        step_dispatch<V, true, false>(buf, nseq, L, steps[j], true, twt, bhat);
+    }
+    for (int j = nstep - 1; j >= 0; --j) step_dispatch<V, false, false>(buf, nseq, L, steps[j], j < nstep - 1, twt, bhat);
+    return;
+  }
+  for (int j = 0; j < nstep; ++j) {
+    if (steps[j].blue)
+      bluestein_step<V>(buf, W, nseq, L, steps[j], j < nstep - 1, steps, twt, tab);
+    else
+      step_dispatch<V, true, false>(buf, nseq, L, steps[j], j < nstep - 1, twt, nullptr);
+  }
 }
 
 // Digit-reversed position of spectrum index k after the DIT steps.
@@ -176,11 +244,11 @@ __device__ __forceinline__ int dit_pos(int k, const FftStep* steps, int nstep) {
   return pos;
 }
 
-// Shared prologue: ring descriptor, steps and the 2-level twiddle table.
+// Shared prologue: ring descriptor, steps (ring + inner) and the twiddle tables.
 struct RingSmem {
   FftRing rg;
   FftWork wk;
-  FftStep st[kMaxSteps];
+  FftStep st[kMaxAllSteps];
   double2 tw[kTwMax];
 };
 
@@ -190,8 +258,8 @@ __device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, int 
     rs.rg = p.rings[rs.wk.ring];
   }
   __syncthreads();
-  if ((int)threadIdx.x < rs.rg.nstep) rs.st[threadIdx.x] = p.steps[rs.rg.step0 + threadIdx.x];
-  for (int t = threadIdx.x; t < rs.rg.ntw; t += blockDim.x) rs.tw[t] = p.tw[rs.rg.tw2_off + t];
+  if ((int)threadIdx.x < kMaxAllSteps) rs.st[threadIdx.x] = p.steps[rs.rg.step0 + threadIdx.x];
+  for (int t = threadIdx.x; t < rs.rg.ntw; t += blockDim.x) rs.tw[t] = p.tw[rs.rg.tw_off + t];
   __syncthreads();
 }
 
@@ -229,8 +297,8 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   const FftRing& rg = rs.rg;
   const int N = rg.n, L = rg.L, M = rg.mcap;
   double2* buf = smc;
-  double2* stg = smc + fft_slots((size_t)rg.nb * L);  // nb == 1: northern F^a, F^b of the current pair
-  const bool blue = rg.chirp_off >= 0;
+  double2* W = smc + fft_slots((size_t)rg.nb * L);  // factor-local Bluestein work buffer
+  const bool blue = rg.chirp_off >= 0;             // whole-ring Bluestein
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
   const double scale = 0.5 / N;
@@ -240,19 +308,21 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
 
   for (int t = 0; t < nbatch; ++t) {
     const Batch bt = batch_of(rg, rs.wk, t);
-    // grid -> smem (cp.async, field a -> .x, field b -> .y), zero tail, chirp
+    // grid -> smem (cp.async, field a -> .x, field b -> .y), zero tail
     for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
       const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
       const int fa = 2 * (bt.pa + (bt.side < 0 ? (q >> 1) : 0));
       const int side = bt.side < 0 ? (q & 1) : bt.side;
       double* dst = reinterpret_cast<double*>(buf + px(idx));
-      if (n < N && !(p.debug & 2)) {
-        const int64_t go = (side ? rg.goff_s : rg.goff_n) + n;
-        cp_async8(dst, grid + (int64_t)fa * p.grid_ld + go);
-        if (fa + 1 < p.nfld)
-          cp_async8(dst + 1, grid + (int64_t)(fa + 1) * p.grid_ld + go);
-        else
-          dst[1] = 0.0;
+      if (n < N) {
+        if (!(p.debug & 2)) {
+          const int64_t go = (side ? rg.goff_s : rg.goff_n) + n;
+          cp_async8(dst, grid + (int64_t)fa * p.grid_ld + go);
+          if (fa + 1 < p.nfld)
+            cp_async8(dst + 1, grid + (int64_t)(fa + 1) * p.grid_ld + go);
+          else
+            dst[1] = 0.0;
+        }
       } else {
         buf[px(idx)] = make_double2(0.0, 0.0);
       }
@@ -267,13 +337,14 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       }
       __syncthreads();
     }
-    if (!(p.debug & 1)) ring_dft<V>(buf, L, bt.nseq, rs.st, rg.nstep, rs.tw, blue, bhat);
+    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, bt.nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
     auto Z = [&](int q, int k) {
       if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]));
       return buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
     };
     auto split = [&](int q, int m, double2& fa, double2& fb) {
-      const double2 zm = Z(q, m), zn = Z(q, m == 0 ? 0 : N - m);
+      const double2 zm = Z(q, m);
+      const double2 zn = Z(q, m == 0 ? 0 : N - m);
       fa = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);
       fb = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);
     };
@@ -295,18 +366,21 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
         }
       }
     } else {
+      // one hemisphere per batch: the northern F^a, F^b wait in the row's S'
+      // slots (same thread writes and re-reads them) until the southern pass
       const int fa = 2 * bt.pa;
       for (int m = threadIdx.x; m <= M; m += NT) {
         double2 xa, xb;
         split(0, m, xa, xb);
+        const int64_t row = p.yrow[rg.yrow_off + m];
+        double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
+        if (p.debug & 4) continue;
         if (bt.side == 0) {
-          stg[2 * m] = xa;
-          stg[2 * m + 1] = xb;
+          d[0] = xa;
+          if (fa + 1 < p.nfld) d[2] = xb;
         } else {
-          const double2 na = stg[2 * m], nbv = stg[2 * m + 1];
-          const int64_t row = p.yrow[rg.yrow_off + m];
-          double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
-          if (p.debug & 4) continue;
+          const double2 na = d[0];
+          const double2 nbv = (fa + 1 < p.nfld) ? d[2] : make_double2(0.0, 0.0);
           __stcs(d, make_double2(w * (na.x + xa.x), w * (na.y + xa.y)));
           __stcs(d + 1, make_double2(w * (na.x - xa.x), w * (na.y - xa.y)));
           if (fa + 1 < p.nfld) {
@@ -331,6 +405,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   const FftRing& rg = rs.rg;
   const int N = rg.n, L = rg.L, M = rg.mcap;
   double2* buf = smc;
+  double2* W = smc + fft_slots((size_t)rg.nb * L);
   const bool blue = rg.chirp_off >= 0;
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
@@ -357,10 +432,10 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       if (!(p.debug & 2)) {
         sa = __ldcs(src);
         aa = __ldcs(src + 1);
-      }
-      if (fa + 1 < p.nfld && !(p.debug & 2)) {
-        sb = __ldcs(src + 2);
-        ab = __ldcs(src + 3);
+        if (fa + 1 < p.nfld) {
+          sb = __ldcs(src + 2);
+          ab = __ldcs(src + 3);
+        }
       }
       for (int side = 0; side < 2; ++side) {
         if (bt.side >= 0 && side != bt.side) continue;
@@ -383,7 +458,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       }
     }
     __syncthreads();
-    if (!(p.debug & 1)) ring_dft<V>(buf, L, bt.nseq, rs.st, rg.nstep, rs.tw, blue, bhat);
+    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, bt.nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
     for (int idx = threadIdx.x; idx < bt.nseq * N; idx += NT) {
       const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
       const int pl = bt.side >= 0 ? 0 : (q >> 1);
@@ -452,32 +527,54 @@ static void group_pencils(const std::vector<int>& primes, std::vector<int>& radi
     if (!placed) bins.push_back(p);
   }
   radices.insert(radices.end(), bins.begin(), bins.end());
-  if (radices.empty()) radices.push_back(1);
 }
 
-int fft_choose(int n, int& variant, std::vector<int>& radices, int& L, bool& bluestein) {
+int fft_bluestein_len(int lo, std::vector<int>& radices) {
   std::vector<int> primes;
-  bluestein = false;
-  if (n >= 2 && n <= kFftMaxLen && factor_primes(n, 31, primes)) {
-    group_pencils(primes, radices);
-    if ((int)radices.size() <= kMaxSteps) {
-      variant = *std::max_element(radices.begin(), radices.end()) > 16 ? 2 : 1;
-      L = n;
-      return 0;
-    }
-  }
-  bluestein = true;
-  for (int cand = 2 * n - 1; cand <= kFftMaxLen; ++cand) {
+  for (int cand = lo; cand <= 4 * lo + 64; ++cand)
     if (factor_primes(cand, 13, primes)) {
       group_pencils(primes, radices);
-      if ((int)radices.size() <= kMaxSteps) {
-        variant = 1;
-        L = cand;
-        return 0;
-      }
+      if ((int)radices.size() <= kMaxSteps) return cand;
+    }
+  return -1;
+}
+
+int fft_plan_ring(int n, RingPlan& rp) {
+  if (n < 2 || n > kFftMaxLen) return SHT_ERR_CONFIG;
+  std::vector<int> primes, small, big;
+  factor_primes(n, n, primes);
+  for (int p : primes) (p > 31 ? big : small).push_back(p);
+  rp.bluestein = !big.empty();
+  rp.ring_blue = false;
+  rp.L = n;
+  rp.wlen = 0;
+  if (rp.bluestein) {  // whole-ring Bluestein when the padded transform fits one CTA
+    std::vector<int> rad;
+    const int L = fft_bluestein_len(2 * n - 1, rad);
+    if (L > 0 && L <= kWholeBluesteinMax) {
+      rp.ring_blue = true;
+      rp.L = L;
+      rp.radices = rad;
+      rp.variant = 1;
+      return SHT_OK;
     }
   }
-  return SHT_ERR_CONFIG;
+  group_pencils(small, rp.radices);
+  rp.variant = 1;
+  for (int r : rp.radices)
+    if (r > 16) rp.variant = 2;
+  int maxLp = 0;
+  for (int p : big) {
+    rp.radices.push_back(p);  // factor-local Bluestein steps last (contiguous pencils)
+    std::vector<int> inner;
+    const int Lp = fft_bluestein_len(2 * p - 1, inner);
+    if (Lp < 0) return SHT_ERR_CONFIG;
+    maxLp = std::max(maxLp, Lp);
+  }
+  rp.wlen = maxLp;  // per pencil; times G by the caller
+  if (rp.radices.empty()) rp.radices.push_back(n);
+  if ((int)rp.radices.size() > kMaxSteps || (int)big.size() > 2) return SHT_ERR_CONFIG;
+  return SHT_OK;
 }
 
 int fft_pos(int k, const std::vector<int>& radices) {
@@ -492,36 +589,132 @@ int fft_pos(int k, const std::vector<int>& radices) {
   return pos;
 }
 
-void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
-               int64_t& tw2_off, int& ntw) {
+static void push_table(std::vector<double2>& arena, int L) {
   const long double two_pi = 6.283185307179586476925286766559005768L;
-  tw2_off = (int64_t)arena.size();
+  auto W = [&](long long e) {
+    const long double a = -two_pi * (long double)(e % L) / (long double)L;
+    return make_double2((double)cosl(a), (double)sinl(a));
+  };
+  for (int e = 0; e < 64; ++e) arena.push_back(W(e));
+  for (int h = 0; h < (L + 63) / 64; ++h) arena.push_back(W(64LL * h));
+}
+
+static FftStep make_step(int L, int B, int R, int tw_base) {
+  FftStep st{};
+  st.R = R;
+  st.B = B;
+  st.S = B / R;
+  st.np = L / R;
+  st.tmul = L / B;
+  st.tw_base = tw_base;
+  st.mag_S = ((uint64_t)1 << 40) / (uint64_t)st.S + 1;
+  st.mag_np = ((uint64_t)1 << 40) / (uint64_t)st.np + 1;
+  st.mag_R = ((uint64_t)1 << 40) / (uint64_t)R + 1;
+  st.chirp_off = st.bhat_off = -1;
+  return st;
+}
+
+void dft_host(const std::vector<std::complex<long double>>& in, std::vector<std::complex<long double>>& out);
+
+int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps, std::vector<double2>& arena,
+                   int64_t& tw_off, int& ntw, int64_t& chirp_off, int64_t& bhat_off) {
+  typedef std::complex<long double> cld;
+  const long double pi_ld = 3.14159265358979323846264338327950288L;
+  const int L = rp.L;
+  tw_off = (int64_t)arena.size();
+  push_table(arena, L);  // ring (or whole-ring Bluestein) table at base 0
+  const size_t first = steps.size();
+  std::vector<FftStep> ring;
   int B = L;
-  for (size_t j = 0; j < radices.size(); ++j) {
-    const int R = radices[j];
-    FftStep st;
-    st.R = R;
-    st.B = B;
-    st.S = B / R;
-    st.np = L / R;
-    st.mag_S = ((uint64_t)1 << 40) / (uint64_t)st.S + 1;
-    st.mag_np = ((uint64_t)1 << 40) / (uint64_t)st.np + 1;
-    st.mag_R = ((uint64_t)1 << 40) / (uint64_t)R + 1;
-    st.tw_lo = st.tw_hi = 0;
-    if (j + 1 < radices.size()) {  // W_B^s = hi[s / 32] lo[s % 32], s < S
-      auto W = [&](long long e) {
-        const long double a = -two_pi * (long double)(e % B) / (long double)B;
-        return make_double2((double)cosl(a), (double)sinl(a));
-      };
-      st.tw_lo = (int)(arena.size() - tw2_off);
-      for (int e = 0; e < 32; ++e) arena.push_back(W(e));
-      st.tw_hi = (int)(arena.size() - tw2_off);
-      for (int h = 0; h < (st.S + 31) / 32; ++h) arena.push_back(W(32LL * h));
-    }
-    out.push_back(st);
-    B = st.S;
+  for (int R : rp.radices) {
+    ring.push_back(make_step(L, B, R, 0));
+    B /= R;
   }
-  ntw = (int)(arena.size() - tw2_off);
+  chirp_off = bhat_off = -1;
+  if (rp.ring_blue) {
+    ntw = (int)((int64_t)arena.size() - tw_off);
+    std::vector<cld> chirp(n);
+    for (int k = 0; k < n; ++k) {
+      const long long qq = ((long long)k * k) % (2LL * n);
+      const long double a = -pi_ld * (long double)qq / (long double)n;
+      chirp[k] = cld(cosl(a), sinl(a));
+    }
+    chirp_off = (int64_t)arena.size();
+    for (int k = 0; k < n; ++k) arena.push_back(make_double2((double)chirp[k].real(), (double)chirp[k].imag()));
+    std::vector<cld> b(L, cld(0)), bh;
+    for (int k = 0; k < n; ++k) {
+      b[k] = std::conj(chirp[k]);
+      if (k) b[L - k] = std::conj(chirp[k]);
+    }
+    dft_host(b, bh);
+    std::vector<double2> perm(L);
+    for (int k = 0; k < L; ++k) {
+      const cld v = bh[k] / (long double)L;
+      perm[fft_pos(k, rp.radices)] = make_double2((double)v.real(), (double)v.imag());
+    }
+    bhat_off = (int64_t)arena.size();
+    arena.insert(arena.end(), perm.begin(), perm.end());
+    steps.insert(steps.end(), ring.begin(), ring.end());
+    while (steps.size() < first + kMaxAllStepsHost) steps.push_back(FftStep{});
+    return ntw > kTwMax ? SHT_ERR_CONFIG : SHT_OK;
+  }
+  // inner plans of the Bluestein steps (their tables follow the ring table)
+  std::vector<FftStep> inner;
+  std::vector<std::pair<size_t, std::vector<int>>> blue_inner;  // ring-step index, inner radices
+  for (size_t j = 0; j < ring.size(); ++j) {
+    FftStep& st = ring[j];
+    if (st.R <= 31) continue;
+    std::vector<int> irad;
+    const int Lp = fft_bluestein_len(2 * st.R - 1, irad);
+    const int base = (int)((int64_t)arena.size() - tw_off);
+    push_table(arena, Lp);
+    st.blue = 1;
+    st.Lp = Lp;
+    st.G = G;
+    st.inner0 = (int)(rp.radices.size() + inner.size());
+    st.ninner = (int)irad.size();
+    st.mag_Lp = ((uint64_t)1 << 40) / (uint64_t)Lp + 1;
+    st.mag_Rb = ((uint64_t)1 << 40) / (uint64_t)st.R + 1;
+    int Bi = Lp;
+    for (int Ri : irad) {
+      inner.push_back(make_step(Lp, Bi, Ri, base));
+      Bi /= Ri;
+    }
+    blue_inner.push_back({j, irad});
+  }
+  ntw = (int)((int64_t)arena.size() - tw_off);
+  if (ntw > kTwMax || ring.size() + inner.size() > (size_t)kMaxAllStepsHost) return SHT_ERR_CONFIG;
+  // chirp and kernel spectrum of each Bluestein step (global arena, offsets absolute)
+  for (auto& bi : blue_inner) {
+    FftStep& st = ring[bi.first];
+    const int P = st.R, Lp = st.Lp;
+    std::vector<cld> chirp(P);
+    for (int r = 0; r < P; ++r) {
+      const long long qq = ((long long)r * r) % (2LL * P);
+      const long double a = -pi_ld * (long double)qq / (long double)P;
+      chirp[r] = cld(cosl(a), sinl(a));
+    }
+    st.chirp_off = (int64_t)arena.size();
+    for (int r = 0; r < P; ++r) arena.push_back(make_double2((double)chirp[r].real(), (double)chirp[r].imag()));
+    std::vector<cld> b(Lp, cld(0)), bh;
+    for (int r = 0; r < P; ++r) {
+      b[r] = std::conj(chirp[r]);
+      if (r) b[Lp - r] = std::conj(chirp[r]);
+    }
+    dft_host(b, bh);
+    std::vector<double2> perm(Lp);
+    for (int k = 0; k < Lp; ++k) {
+      const cld v = bh[k] / (long double)Lp;
+      perm[fft_pos(k, bi.second)] = make_double2((double)v.real(), (double)v.imag());
+    }
+    st.bhat_off = (int64_t)arena.size();
+    arena.insert(arena.end(), perm.begin(), perm.end());
+  }
+  steps.insert(steps.end(), ring.begin(), ring.end());
+  steps.insert(steps.end(), inner.begin(), inner.end());
+  // pad so the device may always read kMaxAllSteps entries from step0
+  while (steps.size() < first + kMaxAllStepsHost) steps.push_back(FftStep{});
+  return SHT_OK;
 }
 
 }  // namespace sht

@@ -65,40 +65,50 @@ size_t leg_inv_smem();
 size_t leg_dir_smem();
 
 // ---------------------------------------------------------------- ring FFTs
-constexpr int kMaxSteps = 4;
-constexpr int kFftMaxLen = 6912;                   // longest transform one CTA handles
-constexpr int kTwMax = 320;                        // per-ring step-twiddle table entries (shared memory)
+constexpr int kMaxSteps = 4;                       // pencil steps per transform (ring or Bluestein inner)
+constexpr int kFftMaxLen = 8192;                   // longest ring one CTA handles
+constexpr int kTwMax = 448;                        // per-ring twiddle-table entries (shared memory)
+constexpr int kMaxAllStepsHost = 3 * 4;           // ring steps + inner steps of up to two Bluestein steps
 
 // One step of the in-place "pencil" FFT of length L = R_0 R_1 ... R_{d-1}:
 // blocks of length B = R_j S, each holding S pencils of R points at stride S.
+// A Bluestein step (prime R > 31) computes its DFT_R pencils as chirp-z
+// convolutions of length Lp in a work buffer, G pencils at a time, with the
+// inner FFT steps inner0 .. inner0 + ninner - 1.
 struct FftStep {
   int32_t R;           // pencil length (radix)
   int32_t S;           // pencil stride = B / R
   int32_t B;           // block length
   int32_t np;          // pencils per sequence = L / R
-  int32_t tw_lo;       // step twiddles W_B^s = hi[s / 32] lo[s % 32]: offsets in the ring's table
-  int32_t tw_hi;
+  int32_t tmul;        // twiddle W_B^(r s) = W^(r s tmul) of the owning transform's table
+  int32_t tw_base;     // offset of that transform's 2-level table (lo[64], hi[...]) in the ring table
   uint64_t mag_S, mag_np, mag_R;  // multiply-shift (>> 40) divisors
+  // Bluestein step only (blue != 0)
+  int32_t blue, Lp, inner0, ninner, G, pad;
+  uint64_t mag_Lp, mag_Rb;  // divisors by Lp and by R
+  int64_t chirp_off;   // w_r = exp(-pi i r^2 / R), r < R
+  int64_t bhat_off;    // inner-FFT spectrum of the chirp kernel / Lp, digit-reversed for the inner plan
 };
 
 struct FftRing {       // one northern ring (and its southern mirror) on this rank
   int32_t n;           // points on the ring
-  int32_t L;           // transform length (n, or the Bluestein length)
+  int32_t L;           // transform length: n, or the whole-ring Bluestein length
   int32_t mcap;        // M_i
   int32_t nstep;
   int32_t step0;       // first step in FftParams::steps
   int32_t K;           // field pairs per batch
   int32_t nb;          // sequences per batch: 2K (both hemispheres) or 1
   int32_t variant;
-  uint64_t mag_L, mag_N, mag_M1;  // multiply-shift (>> 40) divisors for L, n, mcap + 1
-  int64_t chirp_off;   // Bluestein chirp w_n = exp(-pi i n^2 / N), n < N            (-1: none)
-  int64_t bhat_off;    // Bluestein kernel spectrum / L, in the DIT output (digit-reversed) order
+  int32_t wlen;        // Bluestein work-buffer length (complex), 0 if none
+  uint64_t mag_N, mag_M1, mag_L;  // multiply-shift (>> 40) divisors for n, mcap + 1, L
+  int64_t chirp_off;   // whole-ring Bluestein: chirp w_n (n < N) in the arena, -1 if none
+  int64_t bhat_off;    // whole-ring Bluestein: kernel spectrum / L, digit-reversed
   int64_t goff_n;      // offset of the northern ring in the local grid field
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
-  int64_t tw2_off;     // arena offset of this ring's step-twiddle table (ntw entries)
+  int64_t tw_off;      // arena offset of this ring's twiddle table (ntw entries)
   int32_t ntw;
-  int32_t pad2;
+  int32_t pad;
   double w;            // Gaussian weight
 };
 
@@ -122,18 +132,31 @@ struct FftParams {
 
 // Ring-FFT launch classes: 1 = pencils <= 16 points, 256 threads, <= 104 KB
 // (2 CTAs/SM); 2 = pencils up to 31 points (primes 17..31), 1 CTA/SM;
-// 3 = class-1 kernel with up to 216 KB of shared memory (1 CTA/SM).
+// 3 = class-1 kernel with up to 212 KB of shared memory (1 CTA/SM).
 constexpr int kFftVariants = 4;  // index 0 unused
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s);
-// Plan for a ring of n points: kernel variant, pencil radices and transform
-// length (n, or a 13-smooth Bluestein length L >= 2n-1).
-int fft_choose(int n, int& variant, std::vector<int>& radices, int& L, bool& bluestein);
-void fft_steps(int L, const std::vector<int>& radices, std::vector<FftStep>& out, std::vector<double2>& arena,
-               int64_t& tw2_off, int& ntw);
-// Shared-memory complex slots for n FFT points (one pad slot per 16 against bank conflicts).
-__host__ __device__ inline size_t fft_slots(size_t n) { return n + n / 16 + 1; }
+
+// Host plan of one ring length: steps (with Bluestein inner steps appended)
+// and the ring's twiddle / chirp tables appended to the arena.
+struct RingPlan {
+  int variant = 1;
+  bool bluestein = false;      // a prime factor > 31
+  bool ring_blue = false;      // whole-ring Bluestein (transform length L >= 2n-1 fits one CTA)
+  int L = 0;                   // transform length
+  std::vector<int> radices;    // steps (factor-local Bluestein primes last)
+  int wlen = 0;                // factor-local Bluestein: work buffer per pencil (Lp)
+};
+constexpr int kWholeBluesteinMax = 6912;   // longest whole-ring Bluestein transform
+int fft_plan_ring(int n, RingPlan& rp);
+// Appends the ring's steps (and inner steps) to `steps`, its tables to `arena`.
+int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps, std::vector<double2>& arena,
+                   int64_t& tw_off, int& ntw, int64_t& chirp_off, int64_t& bhat_off);
 // Position of DFT output k after the in-place DIT pencil FFT (digit reversal).
 int fft_pos(int k, const std::vector<int>& radices);
+// Shared-memory complex slots for n FFT points (one pad slot per 16 against bank conflicts).
+__host__ __device__ inline size_t fft_slots(size_t n) { return n + n / 16 + 1; }
+// Smallest 13-smooth length >= lo whose pencil plan has <= kMaxSteps steps.
+int fft_bluestein_len(int lo, std::vector<int>& radices);
 
 }  // namespace sht

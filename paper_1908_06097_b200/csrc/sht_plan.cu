@@ -156,6 +156,11 @@ static void dft_rec(const cld* in, int stride, cld* out, int n) {
   }
 }
 
+void dft_host(const std::vector<cld>& in, std::vector<cld>& out) {
+  out.resize(in.size());
+  dft_rec(in.data(), 1, out.data(), (int)in.size());
+}
+
 // ------------------------------------------------------------------ plan
 struct Phase {
   cudaEvent_t ev[10];
@@ -342,7 +347,6 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   const int nlr = (int)p->my_rings.size();
   std::vector<FftRing> rings(nlr);
   std::vector<double2> arena;
-  std::map<int, int64_t> chirp_of_N, bhat_of_N;
   std::vector<int32_t> yrow;
   int64_t go = 0;
   for (int lr = 0; lr < nlr; ++lr) {
@@ -356,7 +360,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   p->grid_ld = go;
   const int npairs = (nfld + 1) / 2;
   // shared memory per CTA: variant 1 runs 2 CTAs/SM, variant 2 one
-  const size_t budget[kFftVariants] = {0, 104 * 1024, 216 * 1024, 216 * 1024};
+  const size_t budget[kFftVariants] = {0, 100 * 1024, 212 * 1024, 212 * 1024};
   std::vector<FftStep> steps;
   std::vector<int64_t> ring_cost(nlr, 0);
   int64_t nfour_local = 0;
@@ -367,79 +371,57 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     R.mcap = g.mcap[i];
     R.w = p->w[i];
     nfour_local += 2 * (int64_t)(R.mcap + 1);
-    std::vector<int> rad;
-    int L = 0, variant = 0;
-    bool blue = false;
-    if (fft_choose(R.n, variant, rad, L, blue))
-      return fail(SHT_ERR_CONFIG, "no FFT plan fits for ring length " + std::to_string(R.n));
-    R.L = L;
-    R.variant = variant;
-    R.mag_L = ((uint64_t)1 << 40) / (uint64_t)L + 1;
+    RingPlan rp;
+    if (fft_plan_ring(R.n, rp))
+      return fail(SHT_ERR_CONFIG, "no FFT plan for ring length " + std::to_string(R.n));
+    int variant = rp.variant;
+    R.L = rp.L;
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
-    R.nstep = (int)rad.size();
-    R.step0 = (int)steps.size();
-    fft_steps(L, rad, steps, arena, R.tw2_off, R.ntw);
-    if (R.ntw > kTwMax) return fail(SHT_ERR_CONFIG, "step-twiddle table too large (N=" + std::to_string(R.n) + ")");
-    const long double pi_ld = 3.14159265358979323846264338327950288L;
-    R.chirp_off = R.bhat_off = -1;
-    if (blue) {
-      const int N = R.n;
-      if (!chirp_of_N.count(N)) {
-        std::vector<cld> chirp(N);
-        for (int n = 0; n < N; ++n) {
-          const long long q = ((long long)n * n) % (2LL * N);
-          const long double a = -pi_ld * (long double)q / (long double)N;
-          chirp[n] = cld(cosl(a), sinl(a));
-        }
-        chirp_of_N[N] = (int64_t)arena.size();
-        for (int n = 0; n < N; ++n) arena.push_back(make_double2((double)chirp[n].real(), (double)chirp[n].imag()));
-        std::vector<cld> b(L, cld(0)), bh(L);
-        for (int n = 0; n < N; ++n) {
-          b[n] = std::conj(chirp[n]);
-          if (n) b[L - n] = std::conj(chirp[n]);
-        }
-        dft_rec(b.data(), 1, bh.data(), L);
-        // stored in the digit-reversed order the DIT steps leave the spectrum in
-        std::vector<double2> perm(L);
-        for (int k = 0; k < L; ++k) {
-          const cld v = bh[k] / (long double)L;
-          perm[fft_pos(k, rad)] = make_double2((double)v.real(), (double)v.imag());
-        }
-        bhat_of_N[N] = (int64_t)arena.size();
-        arena.insert(arena.end(), perm.begin(), perm.end());
-      }
-      R.chirp_off = chirp_of_N[N];
-      R.bhat_off = bhat_of_N[N];
-    }
+    R.mag_L = ((uint64_t)1 << 40) / (uint64_t)R.L + 1;
     R.yrow_off = (int64_t)yrow.size();
     for (int m = 0; m <= R.mcap; ++m) {
       const int s = p->m_owner[m];
       yrow.push_back((int32_t)(ybase[s][i] + p->lm_of_m[m]));
     }
-    // batch: K field pairs with both hemispheres (nb = 2K sequences of L) when
-    // they fit, else one sequence at a time (nb = 1; g2f stages the northern
-    // coefficients, (M+1) x 2 complex)
-    auto smem = [&](int nb) {
-      return (fft_slots((size_t)nb * L) + (nb == 1 ? 2 * (size_t)(R.mcap + 1) : 0)) * sizeof(double2);
+    // batch: K field pairs with both hemispheres (nb = 2K sequences of N) when
+    // they fit, else one sequence at a time (nb = 1); Bluestein rings add a
+    // work buffer of G pencils x Lp
+    const int Lp = rp.wlen;
+    auto smem = [&](int nb, int G) {
+      return (fft_slots((size_t)nb * R.L) + (Lp ? fft_slots((size_t)G * Lp) : 0)) * sizeof(double2);
     };
-    int K = std::min(npairs, 64), nb = 2 * K;
-    while (K > 1 && smem(2 * K) > budget[variant]) nb = 2 * --K;
-    if (smem(nb) > budget[variant]) nb = 1;
-    if (smem(nb) > budget[variant] && variant == 1) {  // one CTA per SM with more shared memory
-      variant = 3;
-      K = std::min(npairs, 64);
-      nb = 2 * K;
-      while (K > 1 && smem(2 * K) > budget[variant]) nb = 2 * --K;
-      if (smem(nb) > budget[variant]) nb = 1;
+    auto fit = [&](size_t bud, int& K, int& nb, int& G) {
+      for (K = std::min(npairs, 64); K >= 1; --K) {
+        nb = 2 * K;
+        G = Lp ? std::min(8, (int)(((bud - std::min(bud, fft_slots((size_t)nb * R.L) * sizeof(double2))) /
+                                    sizeof(double2) * 16 / 17) / std::max(1, Lp))) : 0;
+        if ((Lp == 0 || G >= 1) && smem(nb, G) <= bud) return true;
+      }
+      K = 1;
+      nb = 1;
+      G = Lp ? std::min(8, (int)(((bud - std::min(bud, fft_slots((size_t)R.L) * sizeof(double2))) /
+                                  sizeof(double2) * 16 / 17) / std::max(1, Lp))) : 0;
+      return (Lp == 0 || G >= 1) && smem(nb, G) <= bud;
+    };
+    int K = 1, nb = 1, G = 0;
+    if (!fit(budget[variant], K, nb, G)) {
+      if (variant != 1 || !fit(budget[3], K, nb, G))
+        return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+      variant = 3;  // one CTA per SM with more shared memory
     }
-    if (smem(nb) > budget[variant])
-      return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
+    if (fft_build_ring(R.n, rp, std::max(G, 1), steps, arena, R.tw_off, R.ntw, R.chirp_off, R.bhat_off))
+      return fail(SHT_ERR_CONFIG, "FFT plan tables too large for ring length " + std::to_string(R.n));
+    R.step0 = (int)steps.size() - kMaxAllStepsHost;
+    R.nstep = (int)rp.radices.size();
     R.variant = variant;
     R.K = K;
     R.nb = nb;
-    p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb));
-    ring_cost[lr] = (int64_t)npairs * (2LL * L * R.nstep * (blue ? 2 : 1) + 8LL * R.n);
+    R.wlen = Lp * std::max(G, 1);
+    p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb, G));
+    const int64_t esteps = rp.ring_blue ? 2LL * R.L * (int64_t)rp.radices.size()
+                                        : (int64_t)R.n * ((int64_t)rp.radices.size() + (rp.bluestein ? 6 : 0));
+    ring_cost[lr] = (int64_t)npairs * (2 * esteps + 8LL * R.n);
   }
   // split every ring's field pairs over CTAs so each variant's launch has
   // ~6 CTAs per SM of balanced cost; largest first (LPT)
@@ -681,16 +663,14 @@ int sht_alltoall_order(int nranks, int rank, int32_t* peers) {
 }
 
 int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein) {
-  std::vector<int> rad;
-  int L = 0, variant = 0;
-  bool blue = false;
+  RingPlan rp;
   if (n < 1) return fail(SHT_ERR_CONFIG, "ring length must be >= 1");
-  if (fft_choose(n, variant, rad, L, blue)) return fail(SHT_ERR_CONFIG, "no FFT plan for this length");
+  if (fft_plan_ring(n, rp)) return fail(SHT_ERR_CONFIG, "no FFT plan for this length");
   if (radices)
-    for (size_t k = 0; k < rad.size() && k < 32; ++k) radices[k] = rad[k];
-  if (nstages) *nstages = (int32_t)rad.size();
-  if (fft_len) *fft_len = L;
-  if (bluestein) *bluestein = blue ? 1 : 0;
+    for (size_t k = 0; k < rp.radices.size() && k < 32; ++k) radices[k] = rp.radices[k];
+  if (nstages) *nstages = (int32_t)rp.radices.size();
+  if (fft_len) *fft_len = rp.L;
+  if (bluestein) *bluestein = rp.bluestein ? 1 : 0;
   return SHT_OK;
 }
 

@@ -111,15 +111,19 @@ def test_fft_plans(lib):
 
     p20 = fft_plan_info(20)
     assert p20["length"] == 20 and not p20["bluestein"] and len(p20["radices"]) == 2
-    assert fft_plan_info(2560)["radices"] and len(fft_plan_info(2560)["radices"]) == 3    # 16 x 16 x 10
-    assert not fft_plan_info(2576)["bluestein"]    # 2576 = 2^4 * 7 * 23: direct radix-23 pass
-    big = fft_plan_info(2572)                      # 2572 = 4 * 643 -> Bluestein
+    assert len(fft_plan_info(2560)["radices"]) == 3                 # 16 x 16 x 10
+    assert not fft_plan_info(2576)["bluestein"]                     # 2^4 * 7 * 23: direct radix-23 step
+    big = fft_plan_info(2572)                                       # 4 * 643: whole-ring Bluestein
     assert big["bluestein"] and big["length"] >= 2 * 2572 - 1
-    assert int(np.prod(big["radices"])) == big["length"]
-    for n in range(20, 2600, 4):  # every TCo639 ring
+    assert fft_plan_info(8016)["radices"][-1] == 167                # factor-local Bluestein step (TCo1999)
+    assert fft_plan_info(5476)["radices"][-2:] == [37, 37]          # two Bluestein steps (TCo1999 ring)
+    for n in list(range(20, 2600, 4)) + list(range(2600, 8020, 52)):   # TCo639 .. TCo1999 rings
         info = fft_plan_info(n)
         assert int(np.prod(info["radices"])) == info["length"]
-        assert info["length"] == n or info["bluestein"]
+        if info["length"] != n:                                     # whole-ring Bluestein
+            assert info["bluestein"] and info["length"] >= 2 * n - 1
+        else:
+            assert info["bluestein"] == any(r > 31 for r in info["radices"])
 
 
 def test_errors_map_to_reference_classes(lib):
@@ -136,7 +140,7 @@ def test_errors_map_to_reference_classes(lib):
 
 
 @pytest.mark.parametrize("T,nfld,P", [(79, 10, 1), (639, 548, 1), (639, 548, 2), (639, 548, 4), (639, 548, 8),
-                                      (639, 7, 3), (319, 65, 4), (15, 1, 2)])
+                                      (639, 7, 3), (319, 65, 4), (15, 1, 2), (1279, 548, 8), (1999, 548, 8)])
 def test_plan_validate_host_only(lib, T, nfld, P):
     """Every rank's plan (layouts, FFT plans, shared-memory fits) builds on the host."""
     from paper_1908_06097_b200 import plan_validate
@@ -148,6 +152,6 @@ def test_plan_validate_rejects_unsupported(lib):
     from paper_1908_06097_b200 import ConfigurationError, plan_validate
 
     with pytest.raises(ConfigurationError):
-        plan_validate(1279, 548, 8)          # equator rings > 6912-point Bluestein: not built yet
+        plan_validate(2047, 4, 1)            # rings above 8192 points do not fit one CTA
     with pytest.raises(ConfigurationError):
         plan_validate(79, 0, 1)
