@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--cpu-fields", type=int, default=16, help="fields in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--recompute-legendre", action="store_true",
+                    help="regenerate the P table chunk by chunk every transform (TCo1999 memory mode)")
     return ap.parse_args()
 
 
@@ -226,7 +228,7 @@ def run_ours(args):
     T, nf = args.truncation, args.nfld
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.perf_counter()
-    sh = SHTransform(T, nfld=nf, group=group, profile=True)
+    sh = SHTransform(T, nfld=nf, group=group, profile=True, recompute_legendre=args.recompute_legendre)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
 
@@ -324,6 +326,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
                        "grid": "octahedral", "parallelism": f"m/ring-pair sharded x{world}, NCCL all-to-all",
+                       "legendre": "recomputed per transform" if args.recompute_legendre else "stored table",
                        "l2": "inputs larger than L2 (spectral 1.8 GB, grid 7.3 GB per pair at 1 GPU)"},
             "e2e": e2e,
             "gpu_launches": launches * args.steps,

@@ -58,9 +58,13 @@ struct LegParams {
 
 void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s);
 void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s);
-void launch_leg_poly(int T, int nh, int nlm, const int32_t* lm_m, const int32_t* lm_i0, const int64_t* lm_poff,
-                     const int32_t* lm_kp, const double* mu, const double* sint, double* dmant, int32_t* dexp,
-                     double* ptab, cudaStream_t s);
+// P_m^m start values (X-numbers) of every local wavenumber on every ring.
+void launch_leg_diag(int T, int nh, int nlm, const int32_t* lm_m, const double* sint, double* dmant, int32_t* dexp,
+                     cudaStream_t s);
+// P table rows of local wavenumbers [lm0, lm1) at ptab + lm_poff[lm].
+void launch_leg_poly(int T, int nh, int lm0, int lm1, const int32_t* lm_m, const int32_t* lm_i0,
+                     const int64_t* lm_poff, const int32_t* lm_kp, const double* mu, const double* dmant,
+                     const int32_t* dexp, double* ptab, cudaStream_t s);
 size_t leg_inv_smem();
 size_t leg_dir_smem();
 

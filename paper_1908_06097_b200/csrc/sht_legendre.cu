@@ -441,11 +441,11 @@ __device__ __forceinline__ double eps_nm(int n, int m) {
 
 // One thread per (local m, ring): three-term recurrence in n on the mantissa,
 // shared per-ring exponent, renormalised by 2^-400 above 2^400.
-__global__ void leg_poly_kernel(int T, int nh, const int32_t* __restrict__ lm_m, const int32_t* __restrict__ lm_i0,
+__global__ void leg_poly_kernel(int T, int nh, int lm0, const int32_t* __restrict__ lm_m, const int32_t* __restrict__ lm_i0,
                                 const int64_t* __restrict__ lm_poff, const int32_t* __restrict__ lm_kp,
                                 const double* __restrict__ mu, const double* __restrict__ dmant,
                                 const int32_t* __restrict__ dexp, double* __restrict__ ptab) {
-  const int lm = blockIdx.y;
+  const int lm = lm0 + blockIdx.y;
   const int m = lm_m[lm];
   const int i0 = lm_i0[lm];
   const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -456,6 +456,7 @@ __global__ void leg_poly_kernel(int T, int nh, const int32_t* __restrict__ lm_m,
   const double two400 = 0x1p400, twom400 = 0x1p-400;
   int e = dexp[(int64_t)lm * nh + i];
   double q2 = dmant[(int64_t)lm * nh + i];
+  for (int n = T - m + 1; n < kp; ++n) out[n] = 0.0;  // zero padding (the scratch is reused in recompute mode)
   out[0] = ldexp(q2, e);
   if (m == T) return;
   double q1 = __dmul_rn(__dmul_rn(sqrt(2.0 * m + 3.0), x), q2);
@@ -499,13 +500,18 @@ void launch_leg_dir(const LegParams& p, const double* four, double* spec, int gr
   leg_dir_kernel<<<grid, kLegThreads, leg_dir_smem(), s>>>(p, four, spec);
 }
 
-void launch_leg_poly(int T, int nh, int nlm, const int32_t* lm_m, const int32_t* lm_i0, const int64_t* lm_poff,
-                     const int32_t* lm_kp, const double* mu, const double* sint, double* dmant, int32_t* dexp,
-                     double* ptab, cudaStream_t s) {
+void launch_leg_diag(int T, int nh, int nlm, const int32_t* lm_m, const double* sint, double* dmant, int32_t* dexp,
+                     cudaStream_t s) {
   if (nlm == 0) return;
   leg_diag_kernel<<<(nh + 127) / 128, 128, 0, s>>>(T, nh, sint, nlm, lm_m, dmant, dexp);
-  dim3 grid((nh + 127) / 128, nlm);
-  leg_poly_kernel<<<grid, 128, 0, s>>>(T, nh, lm_m, lm_i0, lm_poff, lm_kp, mu, dmant, dexp, ptab);
+}
+
+void launch_leg_poly(int T, int nh, int lm0, int lm1, const int32_t* lm_m, const int32_t* lm_i0,
+                     const int64_t* lm_poff, const int32_t* lm_kp, const double* mu, const double* dmant,
+                     const int32_t* dexp, double* ptab, cudaStream_t s) {
+  if (lm1 <= lm0) return;
+  dim3 grid((nh + 127) / 128, lm1 - lm0);
+  leg_poly_kernel<<<grid, 128, 0, s>>>(T, nh, lm0, lm_m, lm_i0, lm_poff, lm_kp, mu, dmant, dexp, ptab);
 }
 
 }  // namespace sht

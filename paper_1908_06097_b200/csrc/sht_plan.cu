@@ -209,6 +209,15 @@ struct sht_plan {
   float setup_ms = 0.f;
   int fft_debug = 0;
   int leg_debug = 0;
+  // SHT_FLAG_RECOMPUTE_LEGENDRE: the P table is regenerated chunk by chunk of
+  // wavenumbers into a bounded scratch right before the GEMM tiles that use it
+  struct Chunk {
+    int lm0, lm1, ti0, ti1, td0, td1;
+  };
+  std::vector<Chunk> chunks;
+  int64_t* d_lm_poff_rc = nullptr;   // chunk-relative P offsets
+  double* d_dmant = nullptr;
+  int32_t* d_dexp = nullptr;
 };
 
 namespace sht {
@@ -216,7 +225,7 @@ namespace sht {
 static void free_plan(sht_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
-                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps,
+                  p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -495,25 +504,55 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     for (auto& e : set) SHT_CUDA_TRY(cudaEventCreate(&e));
   p->have_events = true;
 
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_dmant, std::max(1, nlm) * (size_t)nh * sizeof(double)));
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_dexp, std::max(1, nlm) * (size_t)nh * sizeof(int32_t)));
+  SHT_CUDA_TRY(cudaEventRecord(p->ev[8], 0));
+  launch_leg_diag(T, nh, nlm, p->d_lm_m, p->d_sint, p->d_dmant, p->d_dexp, 0);
   if (!(p->flags & SHT_FLAG_RECOMPUTE_LEGENDRE)) {
     SHT_CUDA_TRY(cudaMalloc((void**)&p->d_ptab, std::max<int64_t>(p->ptab_len, 1) * sizeof(double)));
     SHT_CUDA_TRY(cudaMemset(p->d_ptab, 0, std::max<int64_t>(p->ptab_len, 1) * sizeof(double)));
-    double* dmant = nullptr;
-    int32_t* dexp = nullptr;
-    SHT_CUDA_TRY(cudaMalloc((void**)&dmant, std::max(1, nlm) * (size_t)nh * sizeof(double)));
-    SHT_CUDA_TRY(cudaMalloc((void**)&dexp, std::max(1, nlm) * (size_t)nh * sizeof(int32_t)));
-    SHT_CUDA_TRY(cudaEventRecord(p->ev[8], 0));
-    launch_leg_poly(T, nh, nlm, p->d_lm_m, p->d_lm_i0, p->d_lm_poff, p->d_lm_kp, p->d_mu, p->d_sint, dmant, dexp,
+    launch_leg_poly(T, nh, 0, nlm, p->d_lm_m, p->d_lm_i0, p->d_lm_poff, p->d_lm_kp, p->d_mu, p->d_dmant, p->d_dexp,
                     p->d_ptab, 0);
-    SHT_CUDA_TRY(cudaGetLastError());
-    SHT_CUDA_TRY(cudaEventRecord(p->ev[9], 0));
-    SHT_CUDA_TRY(cudaEventSynchronize(p->ev[9]));
-    SHT_CUDA_TRY(cudaEventElapsedTime(&p->setup_ms, p->ev[8], p->ev[9]));
-    cudaFree(dmant);
-    cudaFree(dexp);
   } else {
-    return fail(SHT_ERR_CONFIG, "SHT_FLAG_RECOMPUTE_LEGENDRE is not available in this build yet");
+    // chunks of consecutive wavenumbers whose table fits the scratch budget
+    int64_t budget = (int64_t)256 << 20;  // doubles (2 GB); SHT_RECOMPUTE_CHUNK_MB overrides (tests)
+    if (const char* mb = getenv("SHT_RECOMPUTE_CHUNK_MB")) budget = std::max<int64_t>(1, atoll(mb)) << 17;
+    std::vector<int64_t> rc(nlm);
+    int64_t scratch = 0;
+    for (int lm = 0; lm < nlm;) {
+      sht_plan::Chunk ch{};
+      ch.lm0 = lm;
+      int64_t used = 0;
+      while (lm < nlm) {
+        const int64_t sz = (int64_t)(nh - lm_i0[lm]) * lm_kp[lm];
+        if (used > 0 && used + sz > budget) break;
+        rc[lm] = used;
+        used += sz;
+        ++lm;
+      }
+      ch.lm1 = lm;
+      scratch = std::max(scratch, used);
+      p->chunks.push_back(ch);
+    }
+    // tile ranges of each chunk (both tile lists are wavenumber-major)
+    size_t a = 0, b = 0;
+    for (auto& ch : p->chunks) {
+      ch.ti0 = (int)a;
+      while (a < ti.size() && ti[a].lm < ch.lm1) ++a;
+      ch.ti1 = (int)a;
+      ch.td0 = (int)b;
+      while (b < td.size() && td[b].lm < ch.lm1) ++b;
+      ch.td1 = (int)b;
+    }
+    if (int rc2 = upload(&p->d_lm_poff_rc, rc)) return rc2;
+    SHT_CUDA_TRY(cudaMalloc((void**)&p->d_ptab, std::max<int64_t>(scratch, 1) * sizeof(double)));
+    SHT_CUDA_TRY(cudaMemset(p->d_ptab, 0, std::max<int64_t>(scratch, 1) * sizeof(double)));
+    p->ptab_len = scratch;
   }
+  SHT_CUDA_TRY(cudaGetLastError());
+  SHT_CUDA_TRY(cudaEventRecord(p->ev[9], 0));
+  SHT_CUDA_TRY(cudaEventSynchronize(p->ev[9]));
+  SHT_CUDA_TRY(cudaEventElapsedTime(&p->setup_ms, p->ev[8], p->ev[9]));
 
   if (P > 1) {
     if (!nccl_id) return fail(SHT_ERR_CONFIG, "nranks > 1 needs an NCCL unique id");
@@ -524,7 +563,8 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   return SHT_OK;
 }
 
-static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles, int* counter) {
+static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles, int* counter,
+                            const int64_t* poff = nullptr) {
   LegParams lp;
   lp.T = p->g.T;
   lp.nh = p->g.nh;
@@ -532,7 +572,7 @@ static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles,
   lp.nlm = (int)p->my_m.size();
   lp.lm_m = p->d_lm_m;
   lp.lm_i0 = p->d_lm_i0;
-  lp.lm_poff = p->d_lm_poff;
+  lp.lm_poff = poff ? poff : p->d_lm_poff;
   lp.lm_kp = p->d_lm_kp;
   lp.lm_soff = p->d_lm_soff;
   lp.spec_ld = p->spec_ld;
@@ -740,11 +780,24 @@ int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][0], s));
-  if (p->ntiles_inv) {
-    SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
-    const LegParams lp = leg_params(p, p->d_tiles_inv, p->ntiles_inv, p->d_counter);
-    launch_leg_inv(lp, spec, p->X, std::min(p->nsm, p->ntiles_inv), s);
-    SHT_CUDA_TRY(cudaGetLastError());
+  if (p->chunks.empty()) {
+    if (p->ntiles_inv) {
+      SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
+      const LegParams lp = leg_params(p, p->d_tiles_inv, p->ntiles_inv, p->d_counter);
+      launch_leg_inv(lp, spec, p->X, std::min(p->nsm, p->ntiles_inv), s);
+      SHT_CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    for (const auto& ch : p->chunks) {  // regenerate the P rows of this chunk, then its GEMM tiles
+      launch_leg_poly(p->g.T, p->g.nh, ch.lm0, ch.lm1, p->d_lm_m, p->d_lm_i0, p->d_lm_poff_rc, p->d_lm_kp,
+                      p->d_mu, p->d_dmant, p->d_dexp, p->d_ptab, s);
+      if (ch.ti1 > ch.ti0) {
+        SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
+        const LegParams lp = leg_params(p, p->d_tiles_inv + ch.ti0, ch.ti1 - ch.ti0, p->d_counter, p->d_lm_poff_rc);
+        launch_leg_inv(lp, spec, p->X, std::min(p->nsm, ch.ti1 - ch.ti0), s);
+      }
+      SHT_CUDA_TRY(cudaGetLastError());
+    }
   }
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][1], s));
   if (p->nranks > 1)
@@ -776,11 +829,24 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   if (p->nranks > 1)
     if (int rc = alltoall(p, false, s)) return rc;
   if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][6], s));
-  if (p->ntiles_dir) {
-    SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
-    const LegParams lp = leg_params(p, p->d_tiles_dir, p->ntiles_dir, p->d_counter + 1);
-    launch_leg_dir(lp, p->X, spec, std::min(p->nsm, p->ntiles_dir), s);
-    SHT_CUDA_TRY(cudaGetLastError());
+  if (p->chunks.empty()) {
+    if (p->ntiles_dir) {
+      SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
+      const LegParams lp = leg_params(p, p->d_tiles_dir, p->ntiles_dir, p->d_counter + 1);
+      launch_leg_dir(lp, p->X, spec, std::min(p->nsm, p->ntiles_dir), s);
+      SHT_CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    for (const auto& ch : p->chunks) {
+      launch_leg_poly(p->g.T, p->g.nh, ch.lm0, ch.lm1, p->d_lm_m, p->d_lm_i0, p->d_lm_poff_rc, p->d_lm_kp,
+                      p->d_mu, p->d_dmant, p->d_dexp, p->d_ptab, s);
+      if (ch.td1 > ch.td0) {
+        SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
+        const LegParams lp = leg_params(p, p->d_tiles_dir + ch.td0, ch.td1 - ch.td0, p->d_counter + 1, p->d_lm_poff_rc);
+        launch_leg_dir(lp, p->X, spec, std::min(p->nsm, ch.td1 - ch.td0), s);
+      }
+      SHT_CUDA_TRY(cudaGetLastError());
+    }
   }
   if (prof) {
     SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][7], s));
@@ -795,7 +861,8 @@ int sht_kernel_launches(const sht_plan* p, int* per_pair) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   int fft = 0;
   for (int c = 1; c < kFftVariants; ++c) fft += p->fft_nw[c] > 0;
-  if (per_pair) *per_pair = (p->ntiles_inv > 0) + (p->ntiles_dir > 0) + 2 * fft;
+  const int leg = p->chunks.empty() ? (p->ntiles_inv > 0) + (p->ntiles_dir > 0) : 4 * (int)p->chunks.size();
+  if (per_pair) *per_pair = leg + 2 * fft;
   return SHT_OK;
 }
 

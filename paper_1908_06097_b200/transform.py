@@ -55,8 +55,9 @@ class SHTransform:
     nfld       : number of fields per batch.
     group      : torch.distributed process group (NCCL) to shard over, or None
                  for one GPU.
-    recompute_legendre : recompute P_n^m inside the Legendre GEMMs instead of
-                 storing the table (not in this build: raises ConfigurationError).
+    recompute_legendre : do not store the P_n^m table; regenerate it chunk by
+                 chunk of wavenumbers (bounded 2 GB scratch) right before the
+                 GEMM tiles that use it, every transform (TCo1999 memory mode).
     profile    : record CUDA events around every phase (see ``phase_ms``).
     """
 

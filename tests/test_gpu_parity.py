@@ -164,3 +164,25 @@ def test_native_library_loaded(torch):
     maps = Path("/proc/self/maps").read_text()
     assert str(_lib.LIB_PATH) in maps
     assert lib.sht_version() >= 100
+
+
+def test_recompute_legendre_matches_table(torch, monkeypatch):
+    """SHT_FLAG_RECOMPUTE_LEGENDRE (chunked P regeneration) gives the same
+    transform as the stored table: bitwise, since the table kernel is shared.
+    A 2 MB chunk budget forces dozens of chunks at TCo319."""
+    from oracle.sht_oracle import random_grid, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 319, 5
+    a = torch.from_numpy(random_spectral(T, nf)).cuda()
+    sh = SHTransform(T, nfld=nf)
+    monkeypatch.setenv("SHT_RECOMPUTE_CHUNK_MB", "2")
+    shr = SHTransform(T, nfld=nf, recompute_legendre=True)
+    assert shr.kernel_launches() > 40
+    g = torch.from_numpy(random_grid(T, nf, sh.npts_local)).cuda()
+    assert torch.equal(sh.inv_trans(a), shr.inv_trans(a))
+    assert torch.equal(sh.dir_trans(g), shr.dir_trans(g))
+
+
+def test_parity_tco1279(torch):
+    _check(torch, 1279, 2)

@@ -28,7 +28,7 @@ def main():
     for T, nf in zip(args[0::2], args[1::2]):
         o = SHTransformOracle(T, nfld=nf)
         lay = Layout(o, world)
-        sh = SHTransform(T, nfld=nf, group=dist.group.WORLD)
+        sh = SHTransform(T, nfld=nf, group=dist.group.WORLD, recompute_legendre=bool(int(os.environ.get("SHT_RECOMPUTE", "0"))))
         assert list(sh.m_list) == list(lay.M[rank]), "m partition differs from the restatement"
         assert list(sh.ring_list) == lay.local_rings(rank), "ring partition differs"
         a = random_spectral(T, nf)
