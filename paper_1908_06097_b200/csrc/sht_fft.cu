@@ -2,10 +2,11 @@
 // K5 fft_f2g: Fourier -> grid) on the variable-length octahedral rings.
 //
 // One CTA owns one ring PAIR (northern ring i and its southern mirror, same
-// length N) for a range of field pairs, processed in batches.  Two real
-// fields are packed into one complex sequence (z = x_a + i x_b), so every
-// transform is a complex DFT of length N; the pair is separated with Z_m /
-// conj(Z_{N-m}).
+// length N) for a range of fields, processed in batches of nb fields.  The
+// two hemispheres of a field are packed into one complex sequence
+// (z = x_N + i x_S), so every transform is a complex DFT of length N; the
+// hemispheres are separated with Z_m / conj(Z_{N-m}) and combined at once
+// into the parity rows.
 //
 // The DFT is an in-place "pencil" FFT in shared memory: L = R_0 R_1 ... R_{d-1}
 // (d <= 4, R_j <= 16, or a prime <= 31); in step j every thread owns whole
@@ -14,7 +15,7 @@
 // (base twiddle from a 2-level table in shared memory, powers by recurrence)
 // and writes them back to the same addresses.  No value crosses a barrier in
 // registers and no second buffer is needed, so a 2576-point ring pair for one
-// field pair needs 82 KB and two CTAs share an SM.  The decimation-in-time
+// field needs 82 KB and two CTAs share an SM.  The decimation-in-time
 // order leaves the spectrum digit-reversed (extraction reads it through
 // dit_pos).  A prime factor p > 31 of N becomes a Bluestein step (factor-local
 // chirp-z): its DFT_p pencils are gathered G at a time into a work buffer,
@@ -28,8 +29,10 @@
 // parity rows the Legendre GEMM consumes, S' = w_i (F_N + F_S) and
 // A' = w_i (F_N - F_S) (Gaussian weight folded in).  f2g reads S, A rows and
 // forms F_N = S + A, F_S = S - A while filling its FFT buffer.  Fourier rows
-// are addressed through yrow[] so the same kernels read/write the all-to-all
-// receive/send buffers directly (pack/unpack fused).
+// are addressed through per-(ring, m) row pointers, so g2f stores straight
+// into the m-owner's receive buffer (a peer GPU's memory over NVLink when the
+// transposition runs peer-to-peer) and f2g reads this rank's receive buffer:
+// pack/unpack and the transposition itself are fused.
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -263,29 +266,6 @@ __device__ __forceinline__ void load_ring(RingSmem& rs, const FftParams& p, int 
   __syncthreads();
 }
 
-// Batches: nb == 2K -> K field pairs, sequence q = 2 pl + side; nb == 1 -> one
-// sequence per batch: north then south of each field pair.
-struct Batch {
-  int pa, npr, nseq;   // first field pair, pairs, sequences
-  int side;            // nb == 1: hemisphere of the single sequence
-};
-
-__device__ __forceinline__ Batch batch_of(const FftRing& rg, const FftWork& wk, int t) {
-  Batch b;
-  if (rg.nb > 1) {
-    b.pa = wk.fp0 + t * rg.K;
-    b.npr = min(rg.K, wk.fp1 - b.pa);
-    b.nseq = 2 * b.npr;
-    b.side = -1;
-  } else {
-    b.pa = wk.fp0 + (t >> 1);
-    b.npr = 1;
-    b.nseq = 1;
-    b.side = t & 1;
-  }
-  return b;
-}
-
 // ------------------------------------------------------------------ grid -> Fourier
 template <int V>
 __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
@@ -304,24 +284,20 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   const double scale = 0.5 / N;
   const int64_t rowd = (int64_t)p.nfld * 4;
   const double w = rg.w;
-  const int nbatch = rg.nb > 1 ? (rs.wk.fp1 - rs.wk.fp0 + rg.K - 1) / rg.K : 2 * (rs.wk.fp1 - rs.wk.fp0);
+  const int nbatch = (rs.wk.f1 - rs.wk.f0 + rg.nb - 1) / rg.nb;
 
   for (int t = 0; t < nbatch; ++t) {
-    const Batch bt = batch_of(rg, rs.wk, t);
-    // grid -> smem (cp.async, field a -> .x, field b -> .y), zero tail
-    for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
+    const int fb = rs.wk.f0 + t * rg.nb;
+    const int nseq = min(rg.nb, rs.wk.f1 - fb);
+    // grid -> smem (cp.async, north -> .x, south -> .y), zero tail
+    for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
       const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
-      const int fa = 2 * (bt.pa + (bt.side < 0 ? (q >> 1) : 0));
-      const int side = bt.side < 0 ? (q & 1) : bt.side;
       double* dst = reinterpret_cast<double*>(buf + px(idx));
       if (n < N) {
         if (!(p.debug & 2)) {
-          const int64_t go = (side ? rg.goff_s : rg.goff_n) + n;
-          cp_async8(dst, grid + (int64_t)fa * p.grid_ld + go);
-          if (fa + 1 < p.nfld)
-            cp_async8(dst + 1, grid + (int64_t)(fa + 1) * p.grid_ld + go);
-          else
-            dst[1] = 0.0;
+          const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
+          cp_async8(dst, src + rg.goff_n + n);
+          cp_async8(dst + 1, src + rg.goff_s + n);
         }
       } else {
         buf[px(idx)] = make_double2(0.0, 0.0);
@@ -331,64 +307,28 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     cp_async_wait<0>();
     __syncthreads();
     if (blue) {
-      for (int idx = threadIdx.x; idx < bt.nseq * L; idx += NT) {
+      for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
         const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
         if (n < N) buf[px(idx)] = cmul(buf[px(idx)], __ldg(chirp + n));
       }
       __syncthreads();
     }
-    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, bt.nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
+    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
     auto Z = [&](int q, int k) {
       if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]));
       return buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
     };
-    auto split = [&](int q, int m, double2& fa, double2& fb) {
+    // one thread per (m, field): consecutive threads store consecutive 32-byte
+    // field slots of one Fourier row
+    for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
+      const int m = idx / nseq, q = idx - m * nseq;
       const double2 zm = Z(q, m);
       const double2 zn = Z(q, m == 0 ? 0 : N - m);
-      fa = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);
-      fb = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);
-    };
-    if (bt.side < 0) {
-      for (int idx = threadIdx.x; idx < bt.npr * (M + 1); idx += NT) {
-        const int m = idx / bt.npr, pl = idx - m * bt.npr;
-        double2 na, nbv, sa, sb;
-        split(2 * pl, m, na, nbv);
-        split(2 * pl + 1, m, sa, sb);
-        const int fa = 2 * (bt.pa + pl);
-        const int64_t row = p.yrow[rg.yrow_off + m];
-        double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
-        if (p.debug & 4) continue;
-        __stcs(d, make_double2(w * (na.x + sa.x), w * (na.y + sa.y)));
-        __stcs(d + 1, make_double2(w * (na.x - sa.x), w * (na.y - sa.y)));
-        if (fa + 1 < p.nfld) {
-          __stcs(d + 2, make_double2(w * (nbv.x + sb.x), w * (nbv.y + sb.y)));
-          __stcs(d + 3, make_double2(w * (nbv.x - sb.x), w * (nbv.y - sb.y)));
-        }
-      }
-    } else {
-      // one hemisphere per batch: the northern F^a, F^b wait in the row's S'
-      // slots (same thread writes and re-reads them) until the southern pass
-      const int fa = 2 * bt.pa;
-      for (int m = threadIdx.x; m <= M; m += NT) {
-        double2 xa, xb;
-        split(0, m, xa, xb);
-        const int64_t row = p.yrow[rg.yrow_off + m];
-        double2* d = reinterpret_cast<double2*>(four + row * rowd + (int64_t)fa * 4);
-        if (p.debug & 4) continue;
-        if (bt.side == 0) {
-          d[0] = xa;
-          if (fa + 1 < p.nfld) d[2] = xb;
-        } else {
-          const double2 na = d[0];
-          const double2 nbv = (fa + 1 < p.nfld) ? d[2] : make_double2(0.0, 0.0);
-          __stcs(d, make_double2(w * (na.x + xa.x), w * (na.y + xa.y)));
-          __stcs(d + 1, make_double2(w * (na.x - xa.x), w * (na.y - xa.y)));
-          if (fa + 1 < p.nfld) {
-            __stcs(d + 2, make_double2(w * (nbv.x + xb.x), w * (nbv.y + xb.y)));
-            __stcs(d + 3, make_double2(w * (nbv.x - xb.x), w * (nbv.y - xb.y)));
-          }
-        }
-      }
+      const double2 fn = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);  // F_N
+      const double2 fs = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);  // F_S
+      if (p.debug & 4) continue;
+      st_slot(p.rows_out[rg.yrow_off + m] + (int64_t)(fb + q) * 4, w * (fn.x + fs.x), w * (fn.y + fs.y),
+              w * (fn.x - fs.x), w * (fn.y - fs.y));
     }
     __syncthreads();
   }
@@ -410,66 +350,49 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   const double2* chirp = p.tw + (blue ? rg.chirp_off : 0);
   const double2* bhat = p.tw + (blue ? rg.bhat_off : 0);
   const int64_t rowd = (int64_t)p.nfld * 4;
-  const int nbatch = rg.nb > 1 ? (rs.wk.fp1 - rs.wk.fp0 + rg.K - 1) / rg.K : 2 * (rs.wk.fp1 - rs.wk.fp0);
+  const int nbatch = (rs.wk.f1 - rs.wk.f0 + rg.nb - 1) / rg.nb;
 
   for (int t = 0; t < nbatch; ++t) {
-    const Batch bt = batch_of(rg, rs.wk, t);
+    const int fb = rs.wk.f0 + t * rg.nb;
+    const int nseq = min(rg.nb, rs.wk.f1 - fb);
     // zero the bins no coefficient reaches: (M, N-M) and [N, L)
     const int gap = (N - 2 * M - 1) + (L - N);
-    for (int idx = threadIdx.x; idx < bt.nseq * gap; idx += NT) {
+    for (int idx = threadIdx.x; idx < nseq * gap; idx += NT) {
       const int q = idx / gap, g = idx - q * gap;
       const int k = g < N - 2 * M - 1 ? M + 1 + g : N + (g - (N - 2 * M - 1));
       buf[px(q * L + k)] = make_double2(0.0, 0.0);
     }
-    // Fourier rows -> conj(Z) of both hemispheres at k = m and k = N - m
-    // (one thread per (m, field pair): a row's 64-byte chunks are read once)
-    for (int idx = threadIdx.x; idx < bt.npr * (M + 1); idx += NT) {
-      const int m = idx / bt.npr, pl = idx - m * bt.npr;
-      const int fa = 2 * (bt.pa + pl);
-      const int64_t row = p.yrow[rg.yrow_off + m];
-      const double2* src = reinterpret_cast<const double2*>(four + row * rowd + (int64_t)fa * 4);
-      double2 sa = make_double2(0.0, 0.0), aa = sa, sb = sa, ab = sa;
-      if (!(p.debug & 2)) {
-        sa = __ldcs(src);
-        aa = __ldcs(src + 1);
-        if (fa + 1 < p.nfld) {
-          sb = __ldcs(src + 2);
-          ab = __ldcs(src + 3);
-        }
+    // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
+    // (one thread per (m, field): a row's 32-byte field slots are read once)
+    for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
+      const int m = idx / nseq, q = idx - m * nseq;
+      double2 S = make_double2(0.0, 0.0), A = S;
+      if (!(p.debug & 2)) ld_slot(p.rows_in[rg.yrow_off + m] + (int64_t)(fb + q) * 4, S.x, S.y, A.x, A.y);
+      double2 fn = cadd(S, A), fs = csub(S, A);
+      if (m == 0) {
+        fn.y = 0.0;
+        fs.y = 0.0;
       }
-      for (int side = 0; side < 2; ++side) {
-        if (bt.side >= 0 && side != bt.side) continue;
-        const int q = bt.side >= 0 ? 0 : 2 * pl + side;
-        double2 Fa = side ? csub(sa, aa) : cadd(sa, aa);
-        double2 Fb = side ? csub(sb, ab) : cadd(sb, ab);
-        if (m == 0) {
-          Fa.y = 0.0;
-          Fb.y = 0.0;
-        }
-        // conj(Z) at k = m (Z = Fa + i Fb) and at k = N - m (Z = conj(Fa) + i conj(Fb))
-        double2 lo = make_double2(Fa.x - Fb.y, -(Fa.y + Fb.x));
-        double2 hi = make_double2(Fa.x + Fb.y, Fa.y - Fb.x);
-        if (blue) {
-          lo = cmul(lo, __ldg(chirp + m));
-          if (m) hi = cmul(hi, __ldg(chirp + N - m));
-        }
-        buf[px(q * L + m)] = lo;
-        if (m) buf[px(q * L + N - m)] = hi;
+      // conj(Z) at k = m (Z = F_N + i F_S) and at k = N - m (Z = conj(F_N) + i conj(F_S))
+      double2 lo = make_double2(fn.x - fs.y, -(fn.y + fs.x));
+      double2 hi = make_double2(fn.x + fs.y, fn.y - fs.x);
+      if (blue) {
+        lo = cmul(lo, __ldg(chirp + m));
+        if (m) hi = cmul(hi, __ldg(chirp + N - m));
       }
+      buf[px(q * L + m)] = lo;
+      if (m) buf[px(q * L + N - m)] = hi;
     }
     __syncthreads();
-    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, bt.nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
-    for (int idx = threadIdx.x; idx < bt.nseq * N; idx += NT) {
+    if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
+    for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
       const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
-      const int pl = bt.side >= 0 ? 0 : (q >> 1);
-      const int side = bt.side >= 0 ? bt.side : (q & 1);
       const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]))
                              : buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
-      const int fa = 2 * (bt.pa + pl);
-      const int64_t go = (side ? rg.goff_s : rg.goff_n) + k;
       if (p.debug & 4) continue;
-      __stcs(grid + (int64_t)fa * p.grid_ld + go, r.x);
-      if (fa + 1 < p.nfld) __stcs(grid + (int64_t)(fa + 1) * p.grid_ld + go, -r.y);
+      double* g = grid + (int64_t)(fb + q) * p.grid_ld;
+      __stcs(g + rg.goff_n + k, r.x);
+      __stcs(g + rg.goff_s + k, -r.y);
     }
     __syncthreads();
   }

@@ -11,6 +11,20 @@
 
 namespace sht {
 
+#ifdef __CUDACC__
+// One Fourier-row field slot {S.re, S.im, A.re, A.im} as a single 32-byte
+// access (sm_100 256-bit LDG/STG): full sectors, also over NVLink when the
+// row lives in a peer GPU's buffer.
+__device__ __forceinline__ void st_slot(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_slot(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+#endif
+
 // ---------------------------------------------------------------- error state
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
@@ -48,7 +62,8 @@ struct LegParams {
   const int32_t* lm_kp;      // [nlm] padded P-table row length
   const int64_t* lm_soff;    // [nlm] complex offset of (m, n = m) in the local spectral field
   int64_t spec_ld;           // doubles per local spectral field
-  const int32_t* xbase;      // [nh] Fourier row of (ring i, lm = 0) in the m-side buffer
+  const int32_t* xbase;      // [nh] Fourier row of (ring i, lm = 0) in the m-side buffer (leg_dir)
+  double* const* ring_out;   // [nh] leg_inv: row of (ring i, lm = 0) in the ring owner's receive buffer
   const double* ptab;        // P table
   const LegTile* tiles;
   int ntiles;
@@ -100,8 +115,7 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   int32_t mcap;        // M_i
   int32_t nstep;
   int32_t step0;       // first step in FftParams::steps
-  int32_t K;           // field pairs per batch
-  int32_t nb;          // sequences per batch: 2K (both hemispheres) or 1
+  int32_t nb;          // fields (= complex sequences, north + i south) per batch
   int32_t variant;
   int32_t wlen;        // Bluestein work-buffer length (complex), 0 if none
   uint64_t mag_N, mag_M1, mag_L;  // multiply-shift (>> 40) divisors for n, mcap + 1, L
@@ -116,10 +130,10 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   double w;            // Gaussian weight
 };
 
-struct FftWork {       // one CTA: field pairs [fp0, fp1) of one ring pair
+struct FftWork {       // one CTA: fields [f0, f1) of one ring pair
   int32_t ring;
-  int32_t fp0;
-  int32_t fp1;
+  int32_t f0;
+  int32_t f1;
   int32_t pad;
 };
 
@@ -130,7 +144,8 @@ struct FftParams {
   const FftStep* steps;
   const FftWork* work;
   const double2* tw;         // twiddle / chirp arena
-  const int32_t* yrow;       // Fourier row of (ring, m)
+  double* const* rows_out;   // g2f: Fourier row (field 0) of (ring, m) in the m-owner's receive buffer
+  const double* const* rows_in;  // f2g: Fourier row (field 0) of (ring, m) in this rank's receive buffer
   int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT steps
 };
 

@@ -210,17 +210,14 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       for (int g = 0; g < 4; ++g) {
         const int ring = c.r0 + wr * 32 + g * 8 + lr;
         if (ring < p.nh) {
-          double* dst = four + (int64_t)(p.xbase[ring] + c.lm) * rowd;
+          double* dst = p.ring_out[ring] + (int64_t)c.lm * rowd;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int f = c.f0 + wf * 16 + h * 8 + 2 * lc + e;
-              if (f < p.nfld) {
-                double2* d = reinterpret_cast<double2*>(dst + (int64_t)f * 4);
-                d[0] = make_double2(acc[g][h][0][e], acc[g][h][1][e]);
-                d[1] = make_double2(acc[g][h][2][e], acc[g][h][3][e]);
-              }
+              if (f < p.nfld)
+                st_slot(dst + (int64_t)f * 4, acc[g][h][0][e], acc[g][h][1][e], acc[g][h][2][e], acc[g][h][3][e]);
             }
         }
       }

@@ -198,12 +198,11 @@ struct sht_plan {
   size_t fft_smem[sht::kFftVariants] = {};
   sht::FftStep* d_steps = nullptr;
   double2* d_tw = nullptr;
-  int32_t* d_yrow = nullptr;
   ncclComm_t comm = nullptr;
   bool have_events = false;
   cudaEvent_t ev[10];                      // ev[8], ev[9]: set-up timing
   static constexpr int kHist = 64;         // per-pair phase events of the last kHist pairs
-  cudaEvent_t hist[kHist][8];
+  cudaEvent_t hist[kHist][12];             // (start, end) of inv_leg, inv_a2a, inv_fft, dir_fft, dir_a2a, dir_leg
   bool hist_inv[kHist] = {};               // set k holds the events of an inverse transform
   int hist_cur = 0, hist_done = 0;
   float setup_ms = 0.f;
@@ -218,15 +217,50 @@ struct sht_plan {
   int64_t* d_lm_poff_rc = nullptr;   // chunk-relative P offsets
   double* d_dmant = nullptr;
   int32_t* d_dexp = nullptr;
+  // transposition (SHT_TRANSPORT): "p2p" (default when every peer buffer can
+  // be mapped) fuses it into the kernels -- leg_inv stores each ring's rows
+  // into the ring owner's Y and fft_g2f stores each (ring, m) row into the m
+  // owner's X, over NVLink peer memory -- leaving flag handshakes; "nccl" runs
+  // grouped send/recv of the contiguous row blocks between the kernels.
+  bool p2p = false;
+  std::vector<double*> peer_x, peer_y;          // IPC mappings of the peers' X / Y (own at [rank])
+  std::vector<uint32_t*> peer_flags;            // IPC mappings of the peers' flag words
+  uint32_t* flagw = nullptr;                    // [4][P] written by the peers: kYArr, kXArr, kYFree, kXFree
+  uint32_t** d_peer_flags = nullptr;
+  uint32_t inv_epoch = 0, dir_epoch = 0;
+  std::vector<int32_t> xbase;                   // host copy: X row of (ring, lm = 0)
+  std::vector<int64_t> yrow;                    // per (local ring, m): row in this rank's Y
+  std::vector<int32_t> orow_owner;              // per (local ring, m): owner of m
+  std::vector<int64_t> orow;                    //   and the row in the owner's X
+  std::vector<int64_t> yoff_at_owner;           // per ring owner d: row offset of block r in d's Y
+  double** d_ring_out = nullptr;                // [nh] leg_inv destination row of (ring, lm = 0)
+  double** d_rows_out = nullptr;                // fft_g2f destination row per (local ring, m)
+  const double** d_rows_in = nullptr;           // fft_f2g source row per (local ring, m)
 };
 
 namespace sht {
 
 static void free_plan(sht_plan* p) {
   if (!p) return;
+  if (p->p2p && p->comm) {  // no peer may still store into our buffers or flags
+    cudaDeviceSynchronize();
+    int* d = nullptr;
+    if (cudaMalloc((void**)&d, sizeof(int)) == cudaSuccess) {
+      ncclAllReduce(d, d, 1, ncclInt, ncclSum, p->comm, 0);
+      cudaStreamSynchronize(0);
+      cudaFree(d);
+    }
+  }
+  for (int d = 0; d < (int)p->peer_x.size(); ++d) {
+    if (d == p->rank) continue;
+    if (p->peer_x[d]) cudaIpcCloseMemHandle(p->peer_x[d]);
+    if (p->peer_y[d]) cudaIpcCloseMemHandle(p->peer_y[d]);
+    if (p->peer_flags[d]) cudaIpcCloseMemHandle(p->peer_flags[d]);
+  }
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
                   p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
-                  p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_yrow};
+                  p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->flagw, p->d_peer_flags,
+                  p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_events) {
@@ -250,6 +284,133 @@ static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, 
   if (P < 1) return fail(SHT_ERR_CONFIG, "nranks must be >= 1");
   snake(g.T + 1, P, m_owner);
   snake(g.nh, P, ring_owner);
+  return SHT_OK;
+}
+
+// ------------------------------------------------------------------ transposition
+enum FlagSlot { kYArr = 0, kXArr = 1, kYFree = 2, kXFree = 3 };
+
+// Handshake of the p2p transposition, one thread per peer t: publish
+// `sig_v` in slot `sig_slot` of peer t's flag words (release, system scope:
+// orders every store this GPU made before it in stream order, including the
+// previous kernel's NVLink stores), then wait until peer t has published at
+// least `wait_v` in slot `wait_slot` of ours (acquire).
+__global__ void flag_kernel(uint32_t* const* peer_flags, const uint32_t* flags, int P, int r, int sig_slot,
+                            uint32_t sig_v, int wait_slot, uint32_t wait_v) {
+  const int t = threadIdx.x;
+  if (t >= P || t == r) return;
+  if (sig_slot >= 0) {
+    __threadfence_system();
+    uint32_t* a = peer_flags[t] + sig_slot * P + r;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(sig_v) : "memory");
+  }
+  if (wait_slot >= 0) {
+    const uint32_t* a = flags + wait_slot * P + t;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+      if ((int32_t)(v - wait_v) >= 0) break;
+      __nanosleep(128);
+    }
+  }
+}
+
+static int flags_op(sht_plan* p, int sig_slot, uint32_t sig_v, int wait_slot, uint32_t wait_v, cudaStream_t s) {
+  flag_kernel<<<1, 32 * ((p->nranks + 31) / 32), 0, s>>>(p->d_peer_flags, p->flagw, p->nranks, p->rank, sig_slot,
+                                                          sig_v, wait_slot, wait_v);
+  SHT_CUDA_TRY(cudaGetLastError());
+  return SHT_OK;
+}
+
+// Chooses the transport and builds the row-pointer tables the kernels store
+// through.  p2p: every rank exports X, Y and its flag words (CUDA IPC); the
+// handles travel over the plan's NCCL communicator, and all ranks must map all
+// peers or all fall back to NCCL send/recv.
+static int build_transport(sht_plan* p) {
+  const int P = p->nranks, r = p->rank;
+  const size_t rowd = (size_t)p->nfld * 4;
+  p->peer_x.assign(P, nullptr);
+  p->peer_y.assign(P, nullptr);
+  p->peer_flags.assign(P, nullptr);
+  p->peer_x[r] = p->X;
+  p->peer_y[r] = p->Y;
+  if (P > 1) {
+    const char* tr = getenv("SHT_TRANSPORT");
+    const bool want = !(tr && std::string(tr) == "nccl");
+    SHT_CUDA_TRY(cudaMalloc((void**)&p->flagw, 4 * P * sizeof(uint32_t)));
+    SHT_CUDA_TRY(cudaMemset(p->flagw, 0, 4 * P * sizeof(uint32_t)));
+    p->peer_flags[r] = p->flagw;
+    struct Rec {
+      int32_t ok[16];
+      cudaIpcMemHandle_t h[3];
+    };
+    Rec mine{};
+    mine.ok[0] = want && cudaIpcGetMemHandle(&mine.h[0], p->X) == cudaSuccess &&
+                 cudaIpcGetMemHandle(&mine.h[1], p->Y) == cudaSuccess &&
+                 cudaIpcGetMemHandle(&mine.h[2], p->flagw) == cudaSuccess;
+    cudaGetLastError();
+    Rec* d = nullptr;
+    SHT_CUDA_TRY(cudaMalloc((void**)&d, (P + 1) * sizeof(Rec)));
+    std::vector<Rec> all(P);
+    auto exchange = [&]() -> int {
+      SHT_CUDA_TRY(cudaMemcpy(d + P, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
+      SHT_NCCL_TRY(ncclAllGather(d + P, d, sizeof(Rec), ncclChar, p->comm, 0));
+      SHT_CUDA_TRY(cudaStreamSynchronize(0));
+      SHT_CUDA_TRY(cudaMemcpy(all.data(), d, P * sizeof(Rec), cudaMemcpyDeviceToHost));
+      return SHT_OK;
+    };
+    int rc = exchange();
+    bool ok = rc == SHT_OK;
+    for (int t = 0; t < P && ok; ++t) ok = all[t].ok[0] != 0;
+    if (ok) {  // map every peer, then agree that everybody could
+      for (int t = 0; t < P && ok; ++t) {
+        if (t == r) continue;
+        void *x = nullptr, *y = nullptr, *f = nullptr;
+        ok = cudaIpcOpenMemHandle(&x, all[t].h[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+             cudaIpcOpenMemHandle(&y, all[t].h[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+             cudaIpcOpenMemHandle(&f, all[t].h[2], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+        p->peer_x[t] = (double*)x;
+        p->peer_y[t] = (double*)y;
+        p->peer_flags[t] = (uint32_t*)f;
+      }
+      cudaGetLastError();
+      mine.ok[0] = ok;
+      rc = exchange();
+      ok = rc == SHT_OK;
+      for (int t = 0; t < P && ok; ++t) ok = all[t].ok[0] != 0;
+    }
+    cudaFree(d);
+    if (rc) return rc;
+    p->p2p = ok;
+    if (!ok) {
+      for (int t = 0; t < P; ++t) {
+        if (t == r) continue;
+        if (p->peer_x[t]) cudaIpcCloseMemHandle(p->peer_x[t]);
+        if (p->peer_y[t]) cudaIpcCloseMemHandle(p->peer_y[t]);
+        if (p->peer_flags[t]) cudaIpcCloseMemHandle(p->peer_flags[t]);
+        p->peer_x[t] = p->peer_y[t] = nullptr;
+        p->peer_flags[t] = nullptr;
+      }
+      cudaGetLastError();
+    }
+    if (int rc2 = upload(&p->d_peer_flags, p->peer_flags)) return rc2;
+  }
+  // row pointers: leg_inv's destination per ring, fft_g2f's per (ring, m), fft_f2g's source per (ring, m)
+  const int nh = p->g.nh;
+  std::vector<double*> ring_out(nh), rows_out(p->yrow.size());
+  std::vector<const double*> rows_in(p->yrow.size());
+  for (int i = 0; i < nh; ++i) {
+    const int d = p->ring_owner[i];
+    ring_out[i] = p->p2p ? p->peer_y[d] + (p->xbase[i] - p->xoff[d] + p->yoff_at_owner[d]) * rowd
+                         : p->X + (size_t)p->xbase[i] * rowd;
+  }
+  for (size_t k = 0; k < p->yrow.size(); ++k) {
+    rows_in[k] = p->Y + p->yrow[k] * rowd;
+    rows_out[k] = p->p2p ? p->peer_x[p->orow_owner[k]] + p->orow[k] * rowd : p->Y + p->yrow[k] * rowd;
+  }
+  if (int rc = upload(&p->d_ring_out, ring_out)) return rc;
+  if (int rc = upload(&p->d_rows_out, rows_out)) return rc;
+  if (int rc = upload(&p->d_rows_in, rows_in)) return rc;
   return SHT_OK;
 }
 
@@ -308,6 +469,17 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     p->yrows[s] = cur - p->yoff[s];
   }
   p->ytot = cur;
+  // where this rank's blocks sit in the peers' buffers (p2p transposition):
+  // block r of ring owner d's Y, and block r of m owner t's X
+  p->yoff_at_owner.assign(P, 0);
+  std::vector<int64_t> xoff_at_owner(P, 0);
+  for (int d = 0; d < P; ++d)
+    for (int s2 = 0; s2 < r; ++s2)
+      for (int i : Rlist[d]) p->yoff_at_owner[d] += cnt[s2][i];
+  for (int t = 0; t < P; ++t)
+    for (int d = 0; d < r; ++d)
+      for (int i : Rlist[d]) xoff_at_owner[t] += cnt[t][i];
+  p->xbase = xbase;
   if (p->xtot > INT32_MAX || p->ytot > INT32_MAX) return fail(SHT_ERR_CONFIG, "Fourier row count overflows int32");
 
   // local spectral layout
@@ -356,7 +528,9 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   const int nlr = (int)p->my_rings.size();
   std::vector<FftRing> rings(nlr);
   std::vector<double2> arena;
-  std::vector<int32_t> yrow;
+  p->yrow.clear();
+  p->orow.clear();
+  p->orow_owner.clear();
   int64_t go = 0;
   for (int lr = 0; lr < nlr; ++lr) {
     rings[lr].goff_n = go;
@@ -367,7 +541,6 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     go += g.nloen[p->my_rings[lr]];
   }
   p->grid_ld = go;
-  const int npairs = (nfld + 1) / 2;
   // shared memory per CTA: variant 1 runs 2 CTAs/SM, variant 2 one
   const size_t budget[kFftVariants] = {0, 100 * 1024, 212 * 1024, 212 * 1024};
   std::vector<FftStep> steps;
@@ -388,34 +561,30 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
     R.mag_L = ((uint64_t)1 << 40) / (uint64_t)R.L + 1;
-    R.yrow_off = (int64_t)yrow.size();
+    R.yrow_off = (int64_t)p->yrow.size();
     for (int m = 0; m <= R.mcap; ++m) {
       const int s = p->m_owner[m];
-      yrow.push_back((int32_t)(ybase[s][i] + p->lm_of_m[m]));
+      p->yrow.push_back(ybase[s][i] + p->lm_of_m[m]);
+      p->orow_owner.push_back(s);
+      p->orow.push_back(ybase[s][i] - p->yoff[s] + xoff_at_owner[s] + p->lm_of_m[m]);
     }
-    // batch: K field pairs with both hemispheres (nb = 2K sequences of N) when
-    // they fit, else one sequence at a time (nb = 1); Bluestein rings add a
-    // work buffer of G pencils x Lp
+    // batch: nb fields (one complex sequence of N each, north + i south) as
+    // many as fit; Bluestein rings add a work buffer of G pencils x Lp
     const int Lp = rp.wlen;
     auto smem = [&](int nb, int G) {
       return (fft_slots((size_t)nb * R.L) + (Lp ? fft_slots((size_t)G * Lp) : 0)) * sizeof(double2);
     };
-    auto fit = [&](size_t bud, int& K, int& nb, int& G) {
-      for (K = std::min(npairs, 64); K >= 1; --K) {
-        nb = 2 * K;
+    auto fit = [&](size_t bud, int& nb, int& G) {
+      for (nb = std::min(nfld, 128); nb >= 1; --nb) {
         G = Lp ? std::min(8, (int)(((bud - std::min(bud, fft_slots((size_t)nb * R.L) * sizeof(double2))) /
                                     sizeof(double2) * 16 / 17) / std::max(1, Lp))) : 0;
         if ((Lp == 0 || G >= 1) && smem(nb, G) <= bud) return true;
       }
-      K = 1;
-      nb = 1;
-      G = Lp ? std::min(8, (int)(((bud - std::min(bud, fft_slots((size_t)R.L) * sizeof(double2))) /
-                                  sizeof(double2) * 16 / 17) / std::max(1, Lp))) : 0;
-      return (Lp == 0 || G >= 1) && smem(nb, G) <= bud;
+      return false;
     };
-    int K = 1, nb = 1, G = 0;
-    if (!fit(budget[variant], K, nb, G)) {
-      if (variant != 1 || !fit(budget[3], K, nb, G))
+    int nb = 1, G = 0;
+    if (!fit(budget[variant], nb, G)) {
+      if (variant != 1 || !fit(budget[3], nb, G))
         return fail(SHT_ERR_CONFIG, "ring FFT does not fit in shared memory (N=" + std::to_string(R.n) + ")");
       variant = 3;  // one CTA per SM with more shared memory
     }
@@ -424,15 +593,14 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     R.step0 = (int)steps.size() - kMaxAllStepsHost;
     R.nstep = (int)rp.radices.size();
     R.variant = variant;
-    R.K = K;
     R.nb = nb;
     R.wlen = Lp * std::max(G, 1);
     p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb, G));
     const int64_t esteps = rp.ring_blue ? 2LL * R.L * (int64_t)rp.radices.size()
                                         : (int64_t)R.n * ((int64_t)rp.radices.size() + (rp.bluestein ? 6 : 0));
-    ring_cost[lr] = (int64_t)npairs * (2 * esteps + 8LL * R.n);
+    ring_cost[lr] = (int64_t)nfld * (esteps + 4LL * R.n);
   }
-  // split every ring's field pairs over CTAs so each variant's launch has
+  // split every ring's fields over CTAs so each variant's launch has
   // ~6 CTAs per SM of balanced cost; largest first (LPT)
   std::vector<FftWork> work;
   {
@@ -446,14 +614,14 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
       const double target = std::max<double>(1.0, (double)tot / (6.0 * nsm));
       for (int lr = 0; lr < nlr; ++lr) {
         if (rings[lr].variant != v) continue;
-        const int K = rings[lr].nb > 1 ? rings[lr].K : 1;
-        const int maxsplit = (npairs + K - 1) / K;
+        const int K = rings[lr].nb;
+        const int maxsplit = (nfld + K - 1) / K;
         const int splits = std::max(1, std::min(maxsplit, (int)std::llround(ring_cost[lr] / target)));
-        int chunk = (npairs + splits - 1) / splits;
+        int chunk = (nfld + splits - 1) / splits;
         chunk = (chunk + K - 1) / K * K;
-        for (int a = 0; a < npairs; a += chunk) {
-          const int b = std::min(npairs, a + chunk);
-          wl.push_back({ring_cost[lr] * (b - a) / npairs, {lr, a, b, 0}});
+        for (int a = 0; a < nfld; a += chunk) {
+          const int b = std::min(nfld, a + chunk);
+          wl.push_back({ring_cost[lr] * (b - a) / nfld, {lr, a, b, 0}});
         }
       }
       std::stable_sort(wl.begin(), wl.end(), [](const std::pair<int64_t, FftWork>& x,
@@ -490,7 +658,6 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   if (int rc = upload(&p->d_work, work)) return rc;
   if (int rc = upload(&p->d_steps, steps)) return rc;
   if (int rc = upload(&p->d_tw, arena)) return rc;
-  if (int rc = upload(&p->d_yrow, yrow)) return rc;
   SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
   const size_t rowb = (size_t)nfld * 4 * sizeof(double);
   SHT_CUDA_TRY(cudaMalloc((void**)&p->X, std::max<int64_t>(p->xtot, 1) * rowb));
@@ -560,7 +727,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     std::memcpy(&id, nccl_id, sizeof(id));
     SHT_NCCL_TRY(ncclCommInitRank(&p->comm, P, id, r));
   }
-  return SHT_OK;
+  return build_transport(p);
 }
 
 static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles, int* counter,
@@ -577,6 +744,7 @@ static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles,
   lp.lm_soff = p->d_lm_soff;
   lp.spec_ld = p->spec_ld;
   lp.xbase = p->d_xbase;
+  lp.ring_out = p->d_ring_out;
   lp.ptab = p->d_ptab;
   lp.tiles = tiles;
   lp.ntiles = ntiles;
@@ -593,7 +761,8 @@ static FftParams fft_params(const sht_plan* p) {
   fp.steps = p->d_steps;
   fp.work = p->d_work;
   fp.tw = p->d_tw;
-  fp.yrow = p->d_yrow;
+  fp.rows_out = p->d_rows_out;
+  fp.rows_in = p->d_rows_in;
   fp.debug = p->fft_debug;
   return fp;
 }
@@ -722,12 +891,7 @@ int sht_nccl_get_unique_id(void* out128) {
   return SHT_OK;
 }
 
-int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, int rank, int nranks,
-                    const void* nccl_unique_id, int flags, sht_plan** out) {
-  if (!out) return fail(SHT_ERR_CONFIG, "out is NULL");
-  *out = nullptr;
-  if (nfld < 1) return fail(SHT_ERR_CONFIG, "nfld must be >= 1");
-  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SHT_ERR_CONFIG, "invalid rank / nranks");
+static sht_plan* new_plan(int nfld, int rank, int nranks, int flags) {
   sht_plan* p = new sht_plan();
   p->nfld = nfld;
   p->rank = rank;
@@ -735,6 +899,16 @@ int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, in
   p->flags = flags;
   if (const char* dbg = getenv("SHT_FFT_DEBUG")) p->fft_debug = atoi(dbg);
   if (const char* dbg = getenv("SHT_LEG_DEBUG")) p->leg_debug = atoi(dbg);
+  return p;
+}
+
+int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, int rank, int nranks,
+                    const void* nccl_unique_id, int flags, sht_plan** out) {
+  if (!out) return fail(SHT_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  if (nfld < 1) return fail(SHT_ERR_CONFIG, "nfld must be >= 1");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SHT_ERR_CONFIG, "invalid rank / nranks");
+  sht_plan* p = new_plan(nfld, rank, nranks, flags);
   int rc = make_geometry(truncation, ndgl, nloen, p->g);
   if (!rc) rc = build_plan(p, nccl_unique_id);
   if (rc) {
@@ -773,44 +947,105 @@ int sht_work(const sht_plan* p, double* lf, double* fb, double* ab) {
   return SHT_OK;
 }
 
-int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
-  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
-  if (int rc = check_ptr(spec, "spec")) return rc;
-  if (int rc = check_ptr(grid, "grid")) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][0], s));
+}  // extern "C"
+
+namespace sht {
+
+static void prof_ev(sht_plan* p, int k, cudaStream_t s) {
+  if (p->flags & SHT_FLAG_PROFILE_PHASES) cudaEventRecord(p->hist[p->hist_cur][k], s);
+}
+
+static int phase_leg(sht_plan* p, bool inv, const double* in, double* out, cudaStream_t s) {
+  prof_ev(p, inv ? 0 : 10, s);
+  const LegTile* tiles = inv ? p->d_tiles_inv : p->d_tiles_dir;
+  const int ntiles = inv ? p->ntiles_inv : p->ntiles_dir;
+  int* counter = p->d_counter + (inv ? 0 : 1);
+  auto launch = [&](const LegParams& lp, int n) {
+    if (inv)
+      launch_leg_inv(lp, in, p->X, std::min(p->nsm, n), s);
+    else
+      launch_leg_dir(lp, p->X, out, std::min(p->nsm, n), s);
+  };
   if (p->chunks.empty()) {
-    if (p->ntiles_inv) {
-      SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
-      const LegParams lp = leg_params(p, p->d_tiles_inv, p->ntiles_inv, p->d_counter);
-      launch_leg_inv(lp, spec, p->X, std::min(p->nsm, p->ntiles_inv), s);
-      SHT_CUDA_TRY(cudaGetLastError());
+    if (ntiles) {
+      SHT_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), s));
+      launch(leg_params(p, tiles, ntiles, counter), ntiles);
     }
   } else {
     for (const auto& ch : p->chunks) {  // regenerate the P rows of this chunk, then its GEMM tiles
       launch_leg_poly(p->g.T, p->g.nh, ch.lm0, ch.lm1, p->d_lm_m, p->d_lm_i0, p->d_lm_poff_rc, p->d_lm_kp,
                       p->d_mu, p->d_dmant, p->d_dexp, p->d_ptab, s);
-      if (ch.ti1 > ch.ti0) {
-        SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter, 0, sizeof(int), s));
-        const LegParams lp = leg_params(p, p->d_tiles_inv + ch.ti0, ch.ti1 - ch.ti0, p->d_counter, p->d_lm_poff_rc);
-        launch_leg_inv(lp, spec, p->X, std::min(p->nsm, ch.ti1 - ch.ti0), s);
+      const int t0 = inv ? ch.ti0 : ch.td0, t1 = inv ? ch.ti1 : ch.td1;
+      if (t1 > t0) {
+        SHT_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), s));
+        launch(leg_params(p, tiles + t0, t1 - t0, counter, p->d_lm_poff_rc), t1 - t0);
       }
-      SHT_CUDA_TRY(cudaGetLastError());
     }
   }
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][1], s));
-  if (p->nranks > 1)
-    if (int rc = alltoall(p, true, s)) return rc;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][2], s));
-  const FftParams fp = fft_params(p);
-  for (int c = 1; c < kFftVariants; ++c)
-    launch_fft(false, c, fp, p->fft_w0[c], p->fft_nw[c], p->Y, grid, p->fft_smem[c], s);
   SHT_CUDA_TRY(cudaGetLastError());
-  if (prof) {
-    SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][3], s));
-    p->hist_inv[p->hist_cur] = true;
+  prof_ev(p, inv ? 1 : 11, s);
+  return SHT_OK;
+}
+
+static int phase_a2a(sht_plan* p, bool inv, cudaStream_t s) {
+  prof_ev(p, inv ? 2 : 8, s);
+  if (p->p2p) {  // rows are already in place: publish "mine arrived", wait for everybody's
+    const uint32_t e = inv ? p->inv_epoch : p->dir_epoch;
+    if (int rc = flags_op(p, inv ? kYArr : kXArr, e, inv ? kYArr : kXArr, e, s)) return rc;
+  } else if (p->nranks > 1) {
+    if (int rc = alltoall(p, inv, s)) return rc;
   }
+  prof_ev(p, inv ? 3 : 9, s);
+  return SHT_OK;
+}
+
+static int phase_fft(sht_plan* p, bool inv, const double* in, double* out, cudaStream_t s) {
+  prof_ev(p, inv ? 4 : 6, s);
+  const FftParams fp = fft_params(p);
+  for (int c = 1; c < kFftVariants; ++c) {
+    if (inv)
+      launch_fft(false, c, fp, p->fft_w0[c], p->fft_nw[c], nullptr, out, p->fft_smem[c], s);
+    else
+      launch_fft(true, c, fp, p->fft_w0[c], p->fft_nw[c], in, nullptr, p->fft_smem[c], s);
+  }
+  SHT_CUDA_TRY(cudaGetLastError());
+  prof_ev(p, inv ? 5 : 7, s);
+  return SHT_OK;
+}
+
+static void hist_advance(sht_plan* p, bool inv) {
+  if (!(p->flags & SHT_FLAG_PROFILE_PHASES)) return;
+  if (inv) {
+    p->hist_inv[p->hist_cur] = true;
+  } else {
+    p->hist_cur = (p->hist_cur + 1) % sht_plan::kHist;
+    p->hist_inv[p->hist_cur] = false;
+    p->hist_done = std::min(p->hist_done + 1, sht_plan::kHist);
+  }
+}
+
+}  // namespace sht
+
+extern "C" {
+
+// p2p transposition, per direction with epoch e: wait until every peer has
+// drained the receive buffer this rank stores into (epoch e-1), run the
+// producing kernel (its stores land in the peers' buffers), publish + wait
+// "arrived" (phase_a2a), run the consuming kernel, publish "drained".
+int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (int rc = check_ptr(spec, "spec")) return rc;
+  if (int rc = check_ptr(grid, "grid")) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t e = ++p->inv_epoch;
+  if (p->p2p)
+    if (int rc = flags_op(p, -1, 0, kYFree, e - 1, s)) return rc;
+  if (int rc = phase_leg(p, true, spec, nullptr, s)) return rc;
+  if (int rc = phase_a2a(p, true, s)) return rc;
+  if (int rc = phase_fft(p, true, nullptr, grid, s)) return rc;
+  if (p->p2p)
+    if (int rc = flags_op(p, kYFree, e, -1, 0, s)) return rc;
+  hist_advance(p, true);
   return SHT_OK;
 }
 
@@ -819,41 +1054,15 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   if (int rc = check_ptr(spec, "spec")) return rc;
   if (int rc = check_ptr(grid, "grid")) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  const bool prof = p->flags & SHT_FLAG_PROFILE_PHASES;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][4], s));
-  const FftParams fp = fft_params(p);
-  for (int c = 1; c < kFftVariants; ++c)
-    launch_fft(true, c, fp, p->fft_w0[c], p->fft_nw[c], grid, p->Y, p->fft_smem[c], s);
-  SHT_CUDA_TRY(cudaGetLastError());
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][5], s));
-  if (p->nranks > 1)
-    if (int rc = alltoall(p, false, s)) return rc;
-  if (prof) SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][6], s));
-  if (p->chunks.empty()) {
-    if (p->ntiles_dir) {
-      SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
-      const LegParams lp = leg_params(p, p->d_tiles_dir, p->ntiles_dir, p->d_counter + 1);
-      launch_leg_dir(lp, p->X, spec, std::min(p->nsm, p->ntiles_dir), s);
-      SHT_CUDA_TRY(cudaGetLastError());
-    }
-  } else {
-    for (const auto& ch : p->chunks) {
-      launch_leg_poly(p->g.T, p->g.nh, ch.lm0, ch.lm1, p->d_lm_m, p->d_lm_i0, p->d_lm_poff_rc, p->d_lm_kp,
-                      p->d_mu, p->d_dmant, p->d_dexp, p->d_ptab, s);
-      if (ch.td1 > ch.td0) {
-        SHT_CUDA_TRY(cudaMemsetAsync(p->d_counter + 1, 0, sizeof(int), s));
-        const LegParams lp = leg_params(p, p->d_tiles_dir + ch.td0, ch.td1 - ch.td0, p->d_counter + 1, p->d_lm_poff_rc);
-        launch_leg_dir(lp, p->X, spec, std::min(p->nsm, ch.td1 - ch.td0), s);
-      }
-      SHT_CUDA_TRY(cudaGetLastError());
-    }
-  }
-  if (prof) {
-    SHT_CUDA_TRY(cudaEventRecord(p->hist[p->hist_cur][7], s));
-    p->hist_cur = (p->hist_cur + 1) % sht_plan::kHist;
-    p->hist_inv[p->hist_cur] = false;
-    p->hist_done = std::min(p->hist_done + 1, sht_plan::kHist);
-  }
+  const uint32_t e = ++p->dir_epoch;
+  if (p->p2p)
+    if (int rc = flags_op(p, -1, 0, kXFree, e - 1, s)) return rc;
+  if (int rc = phase_fft(p, false, grid, nullptr, s)) return rc;
+  if (int rc = phase_a2a(p, false, s)) return rc;
+  if (int rc = phase_leg(p, false, nullptr, spec, s)) return rc;
+  if (p->p2p)
+    if (int rc = flags_op(p, kXFree, e, -1, 0, s)) return rc;
+  hist_advance(p, false);
   return SHT_OK;
 }
 
@@ -862,7 +1071,8 @@ int sht_kernel_launches(const sht_plan* p, int* per_pair) {
   int fft = 0;
   for (int c = 1; c < kFftVariants; ++c) fft += p->fft_nw[c] > 0;
   const int leg = p->chunks.empty() ? (p->ntiles_inv > 0) + (p->ntiles_dir > 0) : 4 * (int)p->chunks.size();
-  if (per_pair) *per_pair = leg + 2 * fft;
+  const int sync = p->p2p ? 6 : 0;  // flag handshakes (the NCCL path's kernels are NCCL's)
+  if (per_pair) *per_pair = leg + 2 * fft + sync;
   return SHT_OK;
 }
 
@@ -873,15 +1083,14 @@ int sht_phase_ms_avg(sht_plan* p, int npairs, float* ms, int n) {
   if (!(p->flags & SHT_FLAG_PROFILE_PHASES)) return fail(SHT_ERR_CONFIG, "plan was created without SHT_FLAG_PROFILE_PHASES");
   if (npairs < 1 || npairs > p->hist_done) return fail(SHT_ERR_CONFIG, "npairs must be in [1, completed pairs <= 64]");
   double v[7] = {p->setup_ms, 0, 0, 0, 0, 0, 0};
-  const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}, {6, 7}};
   for (int q = 1; q <= npairs; ++q) {
     const int slot = (p->hist_cur - q + sht_plan::kHist) % sht_plan::kHist;
     cudaEvent_t* e = p->hist[slot];
-    SHT_CUDA_TRY(cudaEventSynchronize(e[7]));
+    SHT_CUDA_TRY(cudaEventSynchronize(e[11]));
     for (int k = 0; k < 6; ++k) {
       if (k < 3 && !p->hist_inv[slot]) continue;  // a direct transform without a preceding inverse
       float t = 0.f;
-      SHT_CUDA_TRY(cudaEventElapsedTime(&t, e[pairs[k][0]], e[pairs[k][1]]));
+      SHT_CUDA_TRY(cudaEventElapsedTime(&t, e[2 * k], e[2 * k + 1]));
       v[k + 1] += t / npairs;
     }
   }
