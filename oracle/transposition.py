@@ -8,8 +8,9 @@ GPU, in process (the reference's oracle-equivalence pattern,
 /root/reference/pkg/tests/test_acceptance.py:60-80: a P-rank run must equal
 the 1-rank oracle) and across real processes over gloo.
 
-* Ownership: snake (boustrophedon) dealing of the zonal wavenumbers m and of
-  the northern ring pairs i over the ranks.
+* Ownership: snake (boustrophedon) dealing of the zonal wavenumbers m
+  (SURVEY.md section 8e); the northern ring pairs i go longest-first to the
+  least-loaded rank under a ring-FFT cost model (ring_fft_cost below).
 * Issue order: rank r sends to (r + k) % P for k = 0..P-1, the reference's
   ROTATED_CONCURRENT schedule (/root/reference/pkg/src/haloflow/
   collectives.py:85-86).
@@ -31,16 +32,75 @@ def snake(n: int, P: int) -> np.ndarray:
     return np.where(blk % 2 == 0, pos, P - 1 - pos).astype(np.int64)
 
 
+def _factor(n: int, maxp: int):
+    primes, m, p = [], n, 2
+    while p <= maxp and m > 1:
+        while m % p == 0:
+            primes.append(p)
+            m //= p
+        p += 1
+    return primes, m == 1
+
+
+def _pencils(primes):
+    """Pencil radices: primes > 16 alone, the rest first-fit-decreasing into factors <= 16."""
+    big = [p for p in primes if p > 16]
+    bins = []
+    for p in sorted((p for p in primes if p <= 16), reverse=True):
+        for j, b in enumerate(bins):
+            if b * p <= 16:
+                bins[j] = b * p
+                break
+        else:
+            bins.append(p)
+    return big + bins
+
+
+def _bluestein_len(lo: int):
+    for cand in range(lo, 4 * lo + 65):
+        primes, ok = _factor(cand, 13)
+        if ok and len(_pencils(primes)) <= 4:
+            return cand, _pencils(primes)
+    return -1, []
+
+
+def ring_fft_cost(n: int, mcap: int) -> int:
+    """Cost of one ring pair's FFTs per field: 3 per element-step + grid and row bytes."""
+    primes, _ = _factor(n, n)
+    big = [p for p in primes if p > 31]
+    if big:
+        L, rad = _bluestein_len(2 * n - 1)
+        if 0 < L <= 6912:
+            return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
+    rad = _pencils([p for p in primes if p <= 31]) + big
+    if not rad:
+        rad = [n]
+    return 3 * n * (len(rad) + (6 if big else 0)) + 16 * n + 32 * (mcap + 1)
+
+
+def ring_partition(nloen_north, mcap_north, P: int) -> np.ndarray:
+    """Longest-processing-time dealing of the ring pairs over P ranks."""
+    cost = [ring_fft_cost(int(n), int(m)) for n, m in zip(nloen_north, mcap_north)]
+    order = sorted(range(len(cost)), key=lambda i: (-cost[i], i))
+    load = [0] * P
+    owner = np.zeros(len(cost), dtype=np.int64)
+    for i in order:
+        r = min(range(P), key=lambda q: (load[q], q))
+        owner[i] = r
+        load[r] += cost[i]
+    return owner
+
+
 class Layout:
     """Ownership and row layout of a P-rank plan (restated)."""
 
     def __init__(self, o: SHTransformOracle, P: int):
         self.o, self.P = o, P
         self.m_owner = snake(o.T + 1, P)
-        self.ring_owner = snake(o.nh, P)
+        self.mcap = o.mcap[: o.nh]
+        self.ring_owner = ring_partition(o.nloen[: o.nh], self.mcap, P)
         self.M = [np.flatnonzero(self.m_owner == r) for r in range(P)]
         self.R = [np.flatnonzero(self.ring_owner == r) for r in range(P)]
-        self.mcap = o.mcap[: o.nh]
 
     def rows(self) -> np.ndarray:
         """rows[r, d]: Fourier rows r sends to d in the inverse transposition."""

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle.sht_oracle import gauss_nodes as oracle_nodes
-from oracle.transposition import Layout, snake
+from oracle.transposition import Layout, ring_fft_cost, ring_partition, snake
 from oracle.sht_oracle import SHTransformOracle
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -59,17 +59,19 @@ def test_partition_matches_restatement(lib, T, P):
     from paper_1908_06097_b200 import partition
 
     mo, ro = partition(T, P)
+    nloen = 4 * np.arange(1, T + 2) + 16
+    mc = np.minimum(T, (nloen - 1) // 2)
     assert np.array_equal(mo, snake(T + 1, P))
-    assert np.array_equal(ro, snake(T + 1, P))
-    # balance: Legendre work within 2% and grid points within 2% across ranks at TCo639
+    assert np.array_equal(ro, ring_partition(nloen, mc, P))
+    # balance at TCo639: Legendre work within 2%, ring-FFT cost within 0.1%, grid points within 3%
     if T == 639:
-        nloen = 4 * np.arange(1, T + 2) + 16
-        mc = np.minimum(T, (nloen - 1) // 2)
         ndglu = np.array([(mc >= m).sum() for m in range(T + 1)])
         work = ndglu * (T - np.arange(T + 1) + 1)
         wr = np.bincount(mo, weights=work, minlength=P)
+        cost = np.array([ring_fft_cost(int(n), int(m)) for n, m in zip(nloen, mc)])
+        cr = np.bincount(ro, weights=cost, minlength=P)
         pr = np.bincount(ro, weights=nloen, minlength=P)
-        assert wr.max() / wr.mean() < 1.02 and pr.max() / pr.mean() < 1.02
+        assert wr.max() / wr.mean() < 1.02 and cr.max() / cr.mean() < 1.001 and pr.max() / pr.mean() < 1.03
 
 
 @pytest.mark.parametrize("T,P", [(15, 2), (79, 3), (639, 8)])
