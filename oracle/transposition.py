@@ -68,8 +68,9 @@ def ring_fft_cost(n: int, mcap: int) -> int:
     """Cost of one ring pair's FFTs per field: 3 per element-step + grid and row bytes."""
     primes, _ = _factor(n, n)
     big = [p for p in primes if p > 31]
-    if big:
-        L, rad = _bluestein_len(2 * n - 1)
+    if big:  # whole-ring Bluestein; even n keeping |k| <= mcap needs only n + 2 mcap lags
+        pruned = n % 2 == 0 and n + 2 * mcap < 2 * n - 1
+        L, rad = _bluestein_len(n + 2 * mcap if pruned else 2 * n - 1)
         if 0 < L <= 6912:
             return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
     rad = _pencils([p for p in primes if p <= 31]) + big

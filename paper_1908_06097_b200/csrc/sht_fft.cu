@@ -314,8 +314,8 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       __syncthreads();
     }
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
-    auto Z = [&](int q, int k) {
-      if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]));
+    auto Z = [&](int q, int k) {  // k = m or N - m (pruned Bluestein: the latter at L - m)
+      if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + (k > M ? k + rg.shift : k))]));
       return buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
     };
     // one thread per (m, field): consecutive threads store consecutive 32-byte
@@ -355,11 +355,11 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   for (int t = 0; t < nbatch; ++t) {
     const int fb = rs.wk.f0 + t * rg.nb;
     const int nseq = min(rg.nb, rs.wk.f1 - fb);
-    // zero the bins no coefficient reaches: (M, N-M) and [N, L)
-    const int gap = (N - 2 * M - 1) + (L - N);
+    // zero the bins no coefficient reaches: (M, N - M + shift) and [N + shift, L)
+    const int gap = L - 2 * M - 1, gap1 = N - 2 * M - 1 + rg.shift;
     for (int idx = threadIdx.x; idx < nseq * gap; idx += NT) {
       const int q = idx / gap, g = idx - q * gap;
-      const int k = g < N - 2 * M - 1 ? M + 1 + g : N + (g - (N - 2 * M - 1));
+      const int k = g < gap1 ? M + 1 + g : N + rg.shift + (g - gap1);
       buf[px(q * L + k)] = make_double2(0.0, 0.0);
     }
     // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
@@ -381,13 +381,13 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
         if (m) hi = cmul(hi, __ldg(chirp + N - m));
       }
       buf[px(q * L + m)] = lo;
-      if (m) buf[px(q * L + N - m)] = hi;
+      if (m) buf[px(q * L + N - m + rg.shift)] = hi;
     }
     __syncthreads();
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
     for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
       const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
-      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + k)]))
+      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + (k ? k + rg.shift : 0))]))
                              : buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
       if (p.debug & 4) continue;
       double* g = grid + (int64_t)(fb + q) * p.grid_ld;
@@ -462,7 +462,7 @@ int fft_bluestein_len(int lo, std::vector<int>& radices) {
   return -1;
 }
 
-int fft_plan_ring(int n, RingPlan& rp) {
+int fft_plan_ring(int n, RingPlan& rp, int mcap) {
   if (n < 2 || n > kFftMaxLen) return SHT_ERR_CONFIG;
   std::vector<int> primes, small, big;
   factor_primes(n, n, primes);
@@ -471,14 +471,23 @@ int fft_plan_ring(int n, RingPlan& rp) {
   rp.ring_blue = false;
   rp.L = n;
   rp.wlen = 0;
+  rp.mcap = -1;
+  rp.shift = 0;
   if (rp.bluestein) {  // whole-ring Bluestein when the padded transform fits one CTA
+    // Chirp-z convolution between n points and the 2 mcap + 1 kept bins
+    // spans n + 2 mcap lags (the chirp is n-periodic for even n), not 2n - 1.
+    const bool pruned = mcap >= 0 && n % 2 == 0 && n + 2 * mcap < 2 * n - 1;
     std::vector<int> rad;
-    const int L = fft_bluestein_len(2 * n - 1, rad);
+    const int L = fft_bluestein_len(pruned ? n + 2 * mcap : 2 * n - 1, rad);
     if (L > 0 && L <= kWholeBluesteinMax) {
       rp.ring_blue = true;
       rp.L = L;
       rp.radices = rad;
       rp.variant = 1;
+      if (pruned) {
+        rp.mcap = mcap;
+        rp.shift = L - n;
+      }
       return SHT_OK;
     }
   }
@@ -564,10 +573,15 @@ int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps
     }
     chirp_off = (int64_t)arena.size();
     for (int k = 0; k < n; ++k) arena.push_back(make_double2((double)chirp[k].real(), (double)chirp[k].imag()));
+    // kernel b_j = conj(chirp_j) at lag j mod L: |j| < n, or (pruned)
+    // j in [-(n + mcap - 1), mcap]
     std::vector<cld> b(L, cld(0)), bh;
-    for (int k = 0; k < n; ++k) {
-      b[k] = std::conj(chirp[k]);
-      if (k) b[L - k] = std::conj(chirp[k]);
+    const long long jlo = rp.mcap >= 0 ? -(long long)(n + rp.mcap - 1) : -(long long)(n - 1);
+    const long long jhi = rp.mcap >= 0 ? rp.mcap : n - 1;
+    for (long long j = jlo; j <= jhi; ++j) {
+      const long long qq = (j * j) % (2LL * n);
+      const long double a = pi_ld * (long double)qq / (long double)n;
+      b[(size_t)((j % L + L) % L)] = cld(cosl(a), sinl(a));
     }
     dft_host(b, bh);
     std::vector<double2> perm(L);

@@ -126,7 +126,7 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
   int64_t tw_off;      // arena offset of this ring's twiddle table (ntw entries)
   int32_t ntw;
-  int32_t pad;
+  int32_t shift;       // pruned whole-ring Bluestein: bins k > M of the spectrum sit at k + L - N (else 0)
   double w;            // Gaussian weight
 };
 
@@ -161,13 +161,16 @@ void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const
 struct RingPlan {
   int variant = 1;
   bool bluestein = false;      // a prime factor > 31
-  bool ring_blue = false;      // whole-ring Bluestein (transform length L >= 2n-1 fits one CTA)
+  bool ring_blue = false;      // whole-ring Bluestein (transform length L fits one CTA)
   int L = 0;                   // transform length
+  int mcap = -1;               // pruned whole-ring Bluestein (even n): only |k| <= mcap is kept,
+  int shift = 0;               //   so L >= n + 2 mcap suffices; negative bins at L - |k| (shift = L - n)
   std::vector<int> radices;    // steps (factor-local Bluestein primes last)
   int wlen = 0;                // factor-local Bluestein: work buffer per pencil (Lp)
 };
 constexpr int kWholeBluesteinMax = 6912;   // longest whole-ring Bluestein transform
-int fft_plan_ring(int n, RingPlan& rp);
+// mcap >= 0: the transform only needs / only feeds the wavenumbers |k| <= mcap
+int fft_plan_ring(int n, RingPlan& rp, int mcap = -1);
 // Appends the ring's steps (and inner steps) to `steps`, its tables to `arena`.
 int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps, std::vector<double2>& arena,
                    int64_t& tw_off, int& ntw, int64_t& chirp_off, int64_t& bhat_off);

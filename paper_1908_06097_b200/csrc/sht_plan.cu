@@ -286,7 +286,7 @@ static int upload(T** dst, const std::vector<T>& v) {
 // Whole-ring Bluestein rings cost ~4x a smooth ring of the same length.
 static int64_t ring_fft_cost(int n, int mcap) {
   RingPlan rp;
-  if (fft_plan_ring(n, rp)) return 16LL * n;
+  if (fft_plan_ring(n, rp, mcap)) return 16LL * n;
   const int64_t ns = (int64_t)rp.radices.size();
   const int64_t esteps = rp.ring_blue ? 2LL * rp.L * ns : (int64_t)n * (ns + (rp.bluestein ? 6 : 0));
   return 3 * esteps + 16LL * n + 32LL * (mcap + 1);
@@ -585,10 +585,11 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     R.w = p->w[i];
     nfour_local += 2 * (int64_t)(R.mcap + 1);
     RingPlan rp;
-    if (fft_plan_ring(R.n, rp))
+    if (fft_plan_ring(R.n, rp, R.mcap))
       return fail(SHT_ERR_CONFIG, "no FFT plan for ring length " + std::to_string(R.n));
     int variant = rp.variant;
     R.L = rp.L;
+    R.shift = rp.shift;
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
     R.mag_L = ((uint64_t)1 << 40) / (uint64_t)R.L + 1;
