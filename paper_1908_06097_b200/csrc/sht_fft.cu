@@ -90,7 +90,8 @@ __device__ __forceinline__ double2 tw_at(const double2* __restrict__ twt, int ba
 
 // One pencil step over nseq sequences of length L (in place).  kFwd: DIT
 // step (codelet, then twiddle); else transposed step (twiddle, then codelet).
-// kPost: last DIT step of a Bluestein convolution: store conj(X * bhat).
+// kPost: last DIT step of a Bluestein convolution fused with the first
+// transposed step (same pencils, no twiddle): store DFT(conj(X * bhat)).
 template <int R, int V, bool kFwd, bool kPost>
 __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, int L, const FftStep& st, bool tw,
                                          const double2* __restrict__ twt, const double2* __restrict__ bhat) {
@@ -131,7 +132,10 @@ __device__ __forceinline__ void step_run(double2* __restrict__ buf, int nseq, in
     if (kPost) {  // last DIT step: S == 1, positions blk * R + r
       const double2* bh = bhat + blk * R;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[px(i0 + r)] = conjc(cmul(v[r], __ldg(bh + r)));
+      for (int r = 0; r < R; ++r) v[r] = conjc(cmul(v[r], __ldg(bh + r)));
+      dft<R>(v);
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[px(i0 + r)] = v[r];
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) buf[px(i0 + r * S)] = v[r];
@@ -192,8 +196,8 @@ __device__ void bluestein_step(double2* __restrict__ buf, double2* __restrict__ 
       else
         step_dispatch<V, true, false>(W, ng, Lp, is, true, twt, bhat);
     }
-    for (int j = st.ninner - 1; j >= 0; --j)
-      step_dispatch<V, false, false>(W, ng, Lp, steps[st.inner0 + j], j < st.ninner - 1, twt, bhat);
+    for (int j = st.ninner - 2; j >= 0; --j)
+      step_dispatch<V, false, false>(W, ng, Lp, steps[st.inner0 + j], true, twt, bhat);
     for (int idx = threadIdx.x; idx < ng * R; idx += NT) {
       const int g = fdiv(idx, st.mag_Rb), k = idx - g * R;
       const int pen = g0 + g;
@@ -222,7 +226,7 @@ __device__ __forceinline__ void ring_dft(double2* buf, double2* W, int L, int ns
       else
         step_dispatch<V, true, false>(buf, nseq, L, steps[j], true, twt, bhat);
     }
-    for (int j = nstep - 1; j >= 0; --j) step_dispatch<V, false, false>(buf, nseq, L, steps[j], j < nstep - 1, twt, bhat);
+    for (int j = nstep - 2; j >= 0; --j) step_dispatch<V, false, false>(buf, nseq, L, steps[j], true, twt, bhat);
     return;
   }
   for (int j = 0; j < nstep; ++j) {
@@ -289,30 +293,37 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
   for (int t = 0; t < nbatch; ++t) {
     const int fb = rs.wk.f0 + t * rg.nb;
     const int nseq = min(rg.nb, rs.wk.f1 - fb);
-    // grid -> smem (cp.async, north -> .x, south -> .y), zero tail
-    for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
-      const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
-      double* dst = reinterpret_cast<double*>(buf + px(idx));
-      if (n < N) {
-        if (!(p.debug & 2)) {
-          const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
-          cp_async8(dst, src + rg.goff_n + n);
-          cp_async8(dst + 1, src + rg.goff_s + n);
-        }
-      } else {
-        buf[px(idx)] = make_double2(0.0, 0.0);
-      }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    // grid -> smem (north -> .x, south -> .y), zero tail; Bluestein rings
+    // apply the chirp on the way (register loads), the others use cp.async
     if (blue) {
+#pragma unroll 4
       for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
         const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
-        if (n < N) buf[px(idx)] = cmul(buf[px(idx)], __ldg(chirp + n));
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N && !(p.debug & 2)) {
+          const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
+          v = cmul(make_double2(__ldcs(src + rg.goff_n + n), __ldcs(src + rg.goff_s + n)), __ldg(chirp + n));
+        }
+        buf[px(idx)] = v;
       }
-      __syncthreads();
+    } else {
+      for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
+        const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
+        double* dst = reinterpret_cast<double*>(buf + px(idx));
+        if (n < N) {
+          if (!(p.debug & 2)) {
+            const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
+            cp_async8(dst, src + rg.goff_n + n);
+            cp_async8(dst + 1, src + rg.goff_s + n);
+          }
+        } else {
+          buf[px(idx)] = make_double2(0.0, 0.0);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
     }
+    __syncthreads();
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
     auto Z = [&](int q, int k) {  // k = m or N - m (pruned Bluestein: the latter at L - m)
       if (blue) return cmul(__ldg(chirp + k), conjc(buf[px(q * L + (k > M ? k + rg.shift : k))]));
