@@ -302,15 +302,34 @@ def run_ours(args):
     B_a2a = max_over_ranks(work["a2a_bytes"], world)
     t_leg_roof = F_leg / (pk["fp64_tflops"] * 1e12) * 1e3
     t_fft_roof = B_fft / (pk["hbm_gbs"] * 1e9) * 1e3
+    transport = sh.transport
     t_a2a_roof = B_a2a / (pk["nvlink_gbs"] * 1e9) * 1e3 if world > 1 else 0.0
-    t_roof = t_leg_roof + t_fft_roof + t_a2a_roof
+    # p2p: the NVLink stores run inside the Legendre / FFT kernels, so the
+    # transfer adds no time of its own to the bound; nccl: it is serialised
+    t_roof = t_leg_roof + t_fft_roof + (t_a2a_roof if transport == "nccl" else 0.0)
 
-    inv_leg, dir_leg = ph["inv_legendre"], ph["dir_legendre"]
-    dom = "leg_inv_kernel" if inv_leg >= dir_leg else "leg_dir_kernel"
-    dom_ms = max(inv_leg, dir_leg)
-    dom_ms = max_over_ranks(dom_ms, world)
-    achieved = (F_leg / 2) / (dom_ms * 1e-3) / 1e12
-    traffic = traffic_per_launch(dom)
+    # per-kernel rooflines (each direction's kernel = one logical launch; the
+    # ring FFT is split over launch classes by shared-memory footprint)
+    def mx(v):
+        return max_over_ranks(v, world)
+
+    kern = {
+        "leg_inv_kernel": ("tensor", mx(ph["inv_legendre"]), F_leg / 2 / 1e12, "TFLOP/s", pk["fp64_tflops"],
+                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop (4*NFLD*sum_m NDGLU(m)(T-m+1) per direction)"),
+        "leg_dir_kernel": ("tensor", mx(ph["dir_legendre"]), F_leg / 2 / 1e12, "TFLOP/s", pk["fp64_tflops"],
+                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop"),
+        "fft_f2g": ("hbm", mx(ph["inv_fft"]), B_fft / 2 / 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
+                    f"{B_fft / 2:.4e} B (grid 8 B x 2 N_i + Fourier rows 32 B x (M_i+1), per field and ring pair)"),
+        "fft_g2f": ("hbm", mx(ph["dir_fft"]), B_fft / 2 / 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
+                    f"{B_fft / 2:.4e} B"),
+    }
+    rooflines = {}
+    for name, (bound, t_ms, amount, unit, peak, src, per) in kern.items():
+        ach = amount / (t_ms * 1e-3) if t_ms > 0 else 0.0
+        rooflines[name] = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit,
+                           "frac": ach / peak, "traffic": traffic_per_launch(name), "ms": t_ms, "peak_src": src,
+                           "per_launch": per}
+    dom = max(rooflines, key=lambda k: rooflines[k]["ms"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -325,18 +344,16 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
-                       "grid": "octahedral", "parallelism": f"m/ring-pair sharded x{world}, NCCL all-to-all",
+                       "grid": "octahedral", "parallelism": f"m/ring-pair sharded x{world}, transposition: {transport}",
                        "legendre": "recomputed per transform" if args.recompute_legendre else "stored table",
                        "l2": "inputs larger than L2 (spectral 1.8 GB, grid 7.3 GB per pair at 1 GPU)"},
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
-            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": pk["fp64_tflops"],
-                         "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"], "traffic": traffic,
-                         "peak_src": pk["fp64_src"],
-                         "per_launch": f"{F_leg / 2:.4e} FP64 flop (4*NFLD*sum_m NDGLU(m)(T-m+1) per direction)"},
+            "roofline": rooflines[dom],
+            "rooflines": rooflines,
             "combined_roofline": {
                 "t_roof_ms": t_roof, "frac": t_roof / ms, "legendre_roof_ms": t_leg_roof,
-                "fft_roof_ms": t_fft_roof, "a2a_roof_ms": t_a2a_roof,
+                "fft_roof_ms": t_fft_roof, "a2a_roof_ms": t_a2a_roof, "transport": transport,
                 "phases_ms": {"legendre": leg_ms, "fft": fft_ms, "alltoall": a2a_ms},
                 "phase_frac": {"legendre_fp64": t_leg_roof / leg_ms if leg_ms else None,
                                "fft_hbm": t_fft_roof / fft_ms if fft_ms else None,

@@ -63,7 +63,9 @@ int sht_version(void);
  * nccl_unique_id: 128 bytes from sht_nccl_get_unique_id() on rank 0, shared
  * by the caller (torch.distributed); NULL when nranks == 1.
  * Replaces the modelled transposition set-up of collectives.build_alltoall
- * (collectives.py:96-117): the plan fixes the size matrix and rotated order. */
+ * (collectives.py:96-117): the plan fixes the size matrix and rotated order,
+ * and (nranks > 1) exchanges the CUDA IPC handles of its receive buffers
+ * over NCCL.  Collective: every rank must call it. */
 int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, int rank, int nranks,
                     const void* nccl_unique_id, int flags, sht_plan** out);
 
@@ -100,9 +102,18 @@ int sht_work(const sht_plan* plan, double* legendre_flops, double* fft_bytes, do
 /* Number of libsht kernel launches one inverse+direct pair issues. */
 int sht_kernel_launches(const sht_plan* plan, int* per_pair);
 
+/* Transport of the grid <-> spectral transposition: *p2p = 1 when the
+ * kernels store the Fourier rows straight into the peers' receive buffers
+ * over NVLink (CUDA IPC mappings, flag handshakes; the default whenever every
+ * rank can map every peer), 0 for NCCL grouped send/recv between the kernels
+ * (SHT_TRANSPORT=nccl, or one rank). */
+int sht_transport(const sht_plan* plan, int* p2p);
+
 /* 128-byte NCCL unique id (call on rank 0 only). */
 int sht_nccl_get_unique_id(void* out128);
 
+/* Collective when nranks > 1 (a barrier over the plan's communicator before
+ * the peer mappings are released). */
 void sht_plan_destroy(sht_plan* plan);
 
 const char* sht_last_error(void);

@@ -25,7 +25,7 @@ SHT_FLAG_PROFILE_PHASES = 2
 # every symbol include/sht.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "sht_version", "sht_plan_create", "sht_inv_trans", "sht_dir_trans", "sht_local_layout",
-    "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
+    "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_transport", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
     "sht_plan_validate", "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
 )
 
@@ -59,6 +59,7 @@ def load() -> C.CDLL:
     lib.sht_phase_ms_avg.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int]
     lib.sht_work.argtypes = [C.c_void_p, f64p, f64p, f64p]
     lib.sht_kernel_launches.argtypes = [C.c_void_p, i32p]
+    lib.sht_transport.argtypes = [C.c_void_p, i32p]
     lib.sht_nccl_get_unique_id.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.restype = None

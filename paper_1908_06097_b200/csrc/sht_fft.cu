@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     };
     // one thread per (m, field): consecutive threads store consecutive 32-byte
     // field slots of one Fourier row
+    #pragma unroll 4
     for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
       const int m = idx / nseq, q = idx - m * nseq;
       const double2 zm = Z(q, m);
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     }
     // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
     // (one thread per (m, field): a row's 32-byte field slots are read once)
+    #pragma unroll 4
     for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
       const int m = idx / nseq, q = idx - m * nseq;
       double2 S = make_double2(0.0, 0.0), A = S;
@@ -396,6 +398,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     }
     __syncthreads();
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
+    #pragma unroll 4
     for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
       const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
       const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + (k ? k + rg.shift : 0))]))

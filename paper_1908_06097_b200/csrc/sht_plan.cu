@@ -1098,6 +1098,12 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   return SHT_OK;
 }
 
+int sht_transport(const sht_plan* p, int* p2p) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (p2p) *p2p = p->p2p ? 1 : 0;
+  return SHT_OK;
+}
+
 int sht_kernel_launches(const sht_plan* p, int* per_pair) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   int fft = 0;

@@ -147,6 +147,14 @@ class SHTransform:
         _lib.check(self._lib.sht_kernel_launches(self._plan, C.byref(n)))
         return int(n.value)
 
+    @property
+    def transport(self) -> str:
+        """'p2p' (rows stored into the peers' buffers by the kernels over NVLink),
+        'nccl' (grouped send/recv) or 'local' (one rank)."""
+        n = C.c_int32()
+        _lib.check(self._lib.sht_transport(self._plan, C.byref(n)))
+        return "p2p" if n.value else ("nccl" if self.nranks > 1 else "local")
+
     def phase_ms(self, npairs: int = 1) -> dict:
         """Device times (ms) per phase, averaged over the last ``npairs`` (<= 64)
         inv_trans + dir_trans pairs (plan created with profile=True)."""

@@ -63,7 +63,7 @@ def test_partition_matches_restatement(lib, T, P):
     mc = np.minimum(T, (nloen - 1) // 2)
     assert np.array_equal(mo, snake(T + 1, P))
     assert np.array_equal(ro, ring_partition(nloen, mc, P))
-    # balance at TCo639: Legendre work within 2%, ring-FFT cost within 0.1%, grid points within 3%
+    # balance at TCo639: Legendre work within 2%, ring-FFT cost within 0.1%, grid points within 5%
     if T == 639:
         ndglu = np.array([(mc >= m).sum() for m in range(T + 1)])
         work = ndglu * (T - np.arange(T + 1) + 1)
@@ -71,7 +71,7 @@ def test_partition_matches_restatement(lib, T, P):
         cost = np.array([ring_fft_cost(int(n), int(m)) for n, m in zip(nloen, mc)])
         cr = np.bincount(ro, weights=cost, minlength=P)
         pr = np.bincount(ro, weights=nloen, minlength=P)
-        assert wr.max() / wr.mean() < 1.02 and cr.max() / cr.mean() < 1.001 and pr.max() / pr.mean() < 1.03
+        assert wr.max() / wr.mean() < 1.02 and cr.max() / cr.mean() < 1.001 and pr.max() / pr.mean() < 1.05
 
 
 @pytest.mark.parametrize("T,P", [(15, 2), (79, 3), (639, 8)])
