@@ -88,10 +88,19 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f,
+                                       "-lms", "50", "-i", str(gpu_index)], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        # do not open the timed region before the sampler is live
+        t0 = time.perf_counter()
+        while self.p is not None and time.perf_counter() - t0 < 5.0:
+            self.f.flush()
+            if Path(self.f.name).stat().st_size > 0:
+                break
+            time.sleep(0.01)
+        self.f.seek(0, os.SEEK_END)
+        self.skip = Path(self.f.name).stat().st_size
 
     def stop(self) -> dict | None:
         if self.p is None:
@@ -99,7 +108,10 @@ class Clocks:
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        txt = Path(self.f.name).read_text()
+        rows = [r.split(",") for r in txt[self.skip:].splitlines() if r.strip()]
+        if not rows:  # a timed region shorter than the sampling period: the sample that bracketed it
+            rows = [r.split(",") for r in txt.splitlines() if r.strip()][-1:]
         os.unlink(self.f.name)
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
