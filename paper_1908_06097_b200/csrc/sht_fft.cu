@@ -296,15 +296,30 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     // grid -> smem (north -> .x, south -> .y), zero tail; Bluestein rings
     // apply the chirp on the way (register loads), the others use cp.async
     if (blue) {
-#pragma unroll 4
-      for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
-        const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
-        double2 v = make_double2(0.0, 0.0);
-        if (n < N && !(p.debug & 2)) {
-          const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
-          v = cmul(make_double2(__ldcs(src + rg.goff_n + n), __ldcs(src + rg.goff_s + n)), __ldg(chirp + n));
+      // 4 elements per thread and round, all 12 loads issued before the first use
+      constexpr int U = 4;
+      const int tot = nseq * L;
+      for (int i0 = threadIdx.x; i0 < tot; i0 += U * NT) {
+        double xn[U], xs[U];
+        double2 c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = i0 + u * NT;
+          const int q = fdiv(idx, rg.mag_L), n = idx - q * L;
+          xn[u] = xs[u] = 0.0;
+          c[u] = make_double2(0.0, 0.0);
+          if (idx < tot && n < N && !(p.debug & 2)) {
+            const double* src = grid + (int64_t)(fb + q) * p.grid_ld;
+            xn[u] = __ldcs(src + rg.goff_n + n);
+            xs[u] = __ldcs(src + rg.goff_s + n);
+            c[u] = __ldg(chirp + n);
+          }
         }
-        buf[px(idx)] = v;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = i0 + u * NT;
+          if (idx < tot) buf[px(idx)] = cmul(make_double2(xn[u], xs[u]), c[u]);
+        }
       }
     } else {
       for (int idx = threadIdx.x; idx < nseq * L; idx += NT) {
@@ -398,15 +413,37 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     }
     __syncthreads();
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
-    #pragma unroll 4
-    for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
-      const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
-      const double2 r = blue ? cmul(__ldg(chirp + k), conjc(buf[px(q * L + (k ? k + rg.shift : 0))]))
-                             : buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
-      if (p.debug & 4) continue;
-      double* g = grid + (int64_t)(fb + q) * p.grid_ld;
-      __stcs(g + rg.goff_n + k, r.x);
-      __stcs(g + rg.goff_s + k, -r.y);
+    if (blue) {  // chirp loads of 4 elements in flight per thread
+      constexpr int U = 4;
+      const int tot = nseq * N;
+      for (int i0 = threadIdx.x; i0 < tot; i0 += U * NT) {
+        double2 c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = i0 + u * NT;
+          const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
+          c[u] = idx < tot ? __ldg(chirp + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = i0 + u * NT;
+          if (idx >= tot || (p.debug & 4)) continue;
+          const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
+          const double2 r = cmul(c[u], conjc(buf[px(q * L + (k ? k + rg.shift : 0))]));
+          double* g = grid + (int64_t)(fb + q) * p.grid_ld;
+          __stcs(g + rg.goff_n + k, r.x);
+          __stcs(g + rg.goff_s + k, -r.y);
+        }
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
+        const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
+        const double2 r = buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
+        if (p.debug & 4) continue;
+        double* g = grid + (int64_t)(fb + q) * p.grid_ld;
+        __stcs(g + rg.goff_n + k, r.x);
+        __stcs(g + rg.goff_s + k, -r.y);
+      }
     }
     __syncthreads();
   }
