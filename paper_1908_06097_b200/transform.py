@@ -214,7 +214,50 @@ class SHTransform:
         """Grid [nfld, npts_local] -> spectral [nfld, nspec_local] (float64)."""
         return self._run(self._lib.sht_dir_trans, grid, self.npts_local, self.nspec_local, out, stream)
 
+    def pairs_pipelined(self, host_in, host_out) -> None:
+        """inv_trans + dir_trans of a stream of host batches: host_in[i] (pinned
+        float64 [nfld, nspec_local]) -> round trip -> host_out[i].  The copy of
+        batch i+1 to the GPU and of batch i-1 back to the host run on their own
+        streams under the transforms of batch i (double-buffered device
+        buffers), so PCIe in, PCIe out and the transform overlap.  Returns when
+        the work is enqueued; the caller's current stream waits for every copy
+        back (synchronize it before reading host_out)."""
+        import torch
+
+        dev = self.device
+        if getattr(self, "_pipe", None) is None:
+            mk = lambda n: torch.empty((self.nfld, n), dtype=torch.float64, device=dev)  # noqa: E731
+            self._pipe = {"din": [mk(self.nspec_local) for _ in range(2)],
+                          "dout": [mk(self.nspec_local) for _ in range(2)], "grid": mk(self.npts_local),
+                          "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev)}
+        P = self._pipe
+        cs = torch.cuda.current_stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        P["h2d"].wait_stream(cs)
+        P["d2h"].wait_stream(cs)
+        for i, (hi, ho) in enumerate(zip(host_in, host_out)):
+            b = i % 2
+            if i >= 2:
+                P["h2d"].wait_event(ev_done[b])   # batch i-2 no longer reads din[b]
+            with torch.cuda.stream(P["h2d"]):
+                P["din"][b].copy_(hi, non_blocking=True)
+            ev_in[b].record(P["h2d"])
+            cs.wait_event(ev_in[b])
+            if i >= 2:
+                cs.wait_event(ev_out[b])          # batch i-2's result has left dout[b]
+            self.inv_trans(P["din"][b], out=P["grid"])
+            self.dir_trans(P["grid"], out=P["dout"][b])
+            ev_done[b].record(cs)
+            P["d2h"].wait_event(ev_done[b])
+            with torch.cuda.stream(P["d2h"]):
+                ho.copy_(P["dout"][b], non_blocking=True)
+            ev_out[b].record(P["d2h"])
+        cs.wait_stream(P["d2h"])
+
     def close(self) -> None:
+        self._pipe = None
         if getattr(self, "_plan", None):
             self._lib.sht_plan_destroy(self._plan)
             self._plan = None

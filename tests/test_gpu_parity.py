@@ -138,6 +138,23 @@ def test_host_arrays_and_streams(torch):
     assert rel(out.cpu().numpy(), o.inv_trans(a)) <= TOL
 
 
+def test_pairs_pipelined_host_stream(torch):
+    """The overlapped host pipeline (bench e2e path) returns each batch's own round trip."""
+    from oracle.sht_oracle import SHTransformOracle, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 63, 5
+    o = SHTransformOracle(T, nfld=nf)
+    sh = SHTransform(T, nfld=nf)
+    ins = [random_spectral(T, nf, seed=100 + i) for i in range(5)]
+    host_in = [torch.from_numpy(x).pin_memory() for x in ins]
+    host_out = [torch.empty(nf, sh.nspec_local, dtype=torch.float64).pin_memory() for _ in ins]
+    sh.pairs_pipelined(host_in, host_out)
+    torch.cuda.synchronize()
+    for x, y in zip(ins, host_out):
+        assert rel(y.numpy(), o.dir_trans(o.inv_trans(x))) <= TOL
+
+
 def test_bad_inputs(torch):
     from paper_1908_06097_b200 import ConfigurationError, SHTransform
 
