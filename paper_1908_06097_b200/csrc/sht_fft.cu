@@ -237,6 +237,24 @@ __device__ __forceinline__ void ring_dft(double2* buf, double2* W, int L, int ns
   }
 }
 
+// Chirp w_k = exp(-i pi k^2 / N) along a thread's walk k = k0, k0 + 256, ...
+// (k0 < 256): w_{k+256} = w_k g_k, g_{k+256} = g_k h, with g_k0 and h from the
+// arena right after the chirp table (fft_build_ring).  Two complex
+// multiplies replace an L2 load per point; ~N/256 steps keep the drift
+// at a few ulp.
+struct ChirpWalk {
+  double2 c, g, h;
+  __device__ __forceinline__ ChirpWalk(const double2* __restrict__ chirp, int N, int k0) {
+    c = k0 < N ? __ldg(chirp + k0) : make_double2(1.0, 0.0);
+    g = __ldg(chirp + N + k0);
+    h = __ldg(chirp + N + 256);
+  }
+  __device__ __forceinline__ void step() {
+    c = cmul(c, g);
+    g = cmul(g, h);
+  }
+};
+
 // Digit-reversed position of spectrum index k after the DIT steps.
 __device__ __forceinline__ int dit_pos(int k, const FftStep* steps, int nstep) {
   int pos = 0;
@@ -295,7 +313,34 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     const int nseq = min(rg.nb, rs.wk.f1 - fb);
     // grid -> smem (north -> .x, south -> .y), zero tail; Bluestein rings
     // apply the chirp on the way (register loads), the others use cp.async
-    if (blue) {
+    if (blue && nseq == 1) {  // one field: thread-strided k with the chirp walked in registers
+      static_assert(NT == 256, "ChirpWalk strides by 256");
+      constexpr int U = 4;
+      const double* src = grid + (int64_t)fb * p.grid_ld;
+      ChirpWalk cw(chirp, N, threadIdx.x);
+      for (int k0 = threadIdx.x; k0 < L; k0 += U * NT) {
+        double xn[U], xs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u * NT;
+          xn[u] = xs[u] = 0.0;
+          if (k < N && !(p.debug & 2)) {
+            xn[u] = __ldcs(src + rg.goff_n + k);
+            xs[u] = __ldcs(src + rg.goff_s + k);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u * NT;
+          if (k < N) {
+            buf[px(k)] = cmul(make_double2(xn[u], xs[u]), cw.c);
+            cw.step();
+          } else if (k < L) {
+            buf[px(k)] = make_double2(0.0, 0.0);
+          }
+        }
+      }
+    } else if (blue) {
       // 4 elements per thread and round, all 12 loads issued before the first use
       constexpr int U = 4;
       const int tot = nseq * L;
@@ -346,6 +391,21 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     };
     // one thread per (m, field): consecutive threads store consecutive 32-byte
     // field slots of one Fourier row
+    if (blue && nseq == 1 && !(p.debug & 4)) {  // chirp walked along m; w_{N-m} = (-1)^N w_m
+      const double sg = (N & 1) ? -1.0 : 1.0;
+      ChirpWalk cw(chirp, N, threadIdx.x);
+      for (int m = threadIdx.x; m <= M; m += NT) {
+        const double2 zm = cmul(cw.c, conjc(buf[px(m)]));
+        const double2 zn = m == 0 ? zm : cmul(make_double2(sg * cw.c.x, sg * cw.c.y), conjc(buf[px(N - m + rg.shift)]));
+        cw.step();
+        const double2 fn = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);  // F_N
+        const double2 fs = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);  // F_S
+        st_slot(p.rows_out[rg.yrow_off + m] + (int64_t)fb * 4, w * (fn.x + fs.x), w * (fn.y + fs.y),
+                w * (fn.x - fs.x), w * (fn.y - fs.y));
+      }
+      __syncthreads();
+      continue;
+    }
     #pragma unroll 4
     for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
       const int m = idx / nseq, q = idx - m * nseq;
@@ -391,6 +451,24 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     }
     // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
     // (one thread per (m, field): a row's 32-byte field slots are read once)
+    if (blue && nseq == 1) {  // chirp walked along m; w_{N-m} = (-1)^N w_m
+      static_assert(NT == 256, "ChirpWalk strides by 256");
+      const double sg = (N & 1) ? -1.0 : 1.0;
+      ChirpWalk cw(chirp, N, threadIdx.x);
+      for (int m = threadIdx.x; m <= M; m += NT) {
+        double2 S = make_double2(0.0, 0.0), A = S;
+        if (!(p.debug & 2)) ld_slot(p.rows_in[rg.yrow_off + m] + (int64_t)fb * 4, S.x, S.y, A.x, A.y);
+        double2 fn = cadd(S, A), fs = csub(S, A);
+        if (m == 0) {
+          fn.y = 0.0;
+          fs.y = 0.0;
+        }
+        const double2 lo = cmul(make_double2(fn.x - fs.y, -(fn.y + fs.x)), cw.c);
+        buf[px(m)] = lo;
+        if (m) buf[px(N - m + rg.shift)] = cmul(make_double2(fn.x + fs.y, fn.y - fs.x), make_double2(sg * cw.c.x, sg * cw.c.y));
+        cw.step();
+      }
+    } else
     #pragma unroll 4
     for (int idx = threadIdx.x; idx < nseq * (M + 1); idx += NT) {
       const int m = idx / nseq, q = idx - m * nseq;
@@ -413,7 +491,17 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     }
     __syncthreads();
     if (!(p.debug & 1)) ring_dft<V>(buf, W, L, nseq, rs.st, rg.nstep, rs.tw, p.tw, blue, bhat);
-    if (blue) {  // chirp loads of 4 elements in flight per thread
+    if (blue && nseq == 1) {  // chirp walked along k
+      ChirpWalk cw(chirp, N, threadIdx.x);
+      double* g = grid + (int64_t)fb * p.grid_ld;
+      for (int k = threadIdx.x; k < N; k += NT) {
+        const double2 r = cmul(cw.c, conjc(buf[px(k ? k + rg.shift : 0)]));
+        cw.step();
+        if (p.debug & 4) continue;
+        __stcs(g + rg.goff_n + k, r.x);
+        __stcs(g + rg.goff_s + k, -r.y);
+      }
+    } else if (blue) {  // chirp loads of 4 elements in flight per thread
       constexpr int U = 4;
       const int tot = nseq * N;
       for (int i0 = threadIdx.x; i0 < tot; i0 += U * NT) {
@@ -624,6 +712,13 @@ int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps
     }
     chirp_off = (int64_t)arena.size();
     for (int k = 0; k < n; ++k) arena.push_back(make_double2((double)chirp[k].real(), (double)chirp[k].imag()));
+    // ChirpWalk factors: g_t = exp(-i pi (512 t + 65536) / n), t < 256, then h = exp(-i pi 131072 / n)
+    auto cis_n = [&](long long num) {
+      const long double a = -pi_ld * (long double)(num % (2LL * n)) / (long double)n;
+      return make_double2((double)cosl(a), (double)sinl(a));
+    };
+    for (int t = 0; t < 256; ++t) arena.push_back(cis_n(512LL * t + 65536LL));
+    arena.push_back(cis_n(131072LL));
     // kernel b_j = conj(chirp_j) at lag j mod L: |j| < n, or (pruned)
     // j in [-(n + mcap - 1), mcap]
     std::vector<cld> b(L, cld(0)), bh;
