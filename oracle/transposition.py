@@ -56,8 +56,35 @@ def _pencils(primes):
     return big + bins
 
 
-def _bluestein_len(lo: int):
-    for cand in range(lo, 4 * lo + 65):
+_CODELET = {2: 4, 3: 12, 4: 16, 5: 36, 6: 44, 7: 66, 8: 55, 9: 88, 10: 108, 11: 150, 12: 128, 13: 204, 14: 184,
+            15: 200, 16: 165}
+
+
+def _bluestein_cost(L: int, rad) -> int:
+    c = 0
+    for j, R in enumerate(rad):
+        pen = L // R
+        c += pen * (2 * _CODELET[R] + 16 * R)
+        if j < len(rad) - 1:
+            c += pen * 2 * (8 * R - 8)
+    return c
+
+
+def _bluestein_len(lo: int, lmax: int = 1 << 30):
+    """Least modelled-cost 13-smooth length in [lo, min(lmax, 1.5 lo)] with <= 4 pencil steps,
+    else the shortest up to min(lmax, 4 lo + 64) (libsht's fft_bluestein_len)."""
+    best = None
+    for cand in range(lo, min(lmax, lo + lo // 2) + 1):
+        primes, ok = _factor(cand, 13)
+        if ok:
+            rad = _pencils(primes)
+            if len(rad) <= 4:
+                c = _bluestein_cost(cand, rad)
+                if best is None or c < best[0]:
+                    best = (c, cand, rad)
+    if best is not None:
+        return best[1], best[2]
+    for cand in range(lo, min(lmax, 4 * lo + 64) + 1):
         primes, ok = _factor(cand, 13)
         if ok and len(_pencils(primes)) <= 4:
             return cand, _pencils(primes)
@@ -70,7 +97,10 @@ def ring_fft_cost(n: int, mcap: int) -> int:
     big = [p for p in primes if p > 31]
     if big:  # whole-ring Bluestein; even n keeping |k| <= mcap needs only n + 2 mcap lags
         pruned = n % 2 == 0 and n + 2 * mcap < 2 * n - 1
-        L, rad = _bluestein_len(n + 2 * mcap if pruned else 2 * n - 1)
+        lo = n + 2 * mcap if pruned else 2 * n - 1
+        L, rad = _bluestein_len(lo, 6022)
+        if L < 0:
+            L, rad = _bluestein_len(lo, 6912)
         if 0 < L <= 6912:
             return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
     rad = _pencils([p for p in primes if p <= 31]) + big

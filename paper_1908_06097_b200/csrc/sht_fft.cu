@@ -591,9 +591,45 @@ static void group_pencils(const std::vector<int>& primes, std::vector<int>& radi
   radices.insert(radices.end(), bins.begin(), bins.end());
 }
 
-int fft_bluestein_len(int lo, std::vector<int>& radices) {
-  std::vector<int> primes;
-  for (int cand = lo; cand <= 4 * lo + 64; ++cand)
+// Modelled cost of a Bluestein convolution of length L with pencil radices
+// `rad` (forward DIT + transposed pass): per pencil the codelet's FP64
+// instructions (SASS count of tools/gen_codelets.py output), the twiddle
+// recurrence (8R - 8, every step but the last) and ~8 instructions of
+// addressing / shared-memory traffic per point.
+static int64_t bluestein_cost(int L, const std::vector<int>& rad) {
+  static const int kCodelet[17] = {0, 0, 4, 12, 16, 36, 44, 66, 55, 88, 108, 150, 128, 204, 184, 200, 165};
+  int64_t c = 0;
+  const int n = (int)rad.size();
+  for (int j = 0; j < n; ++j) {
+    const int R = rad[j];
+    const int64_t pen = L / R;
+    c += pen * (2LL * kCodelet[R] + 16LL * R);
+    if (j < n - 1) c += pen * 2LL * (8 * R - 8);
+  }
+  return c;
+}
+
+// Bluestein length for a convolution spanning `lo` lags: the 13-smooth
+// length in [lo, min(lmax, 3 lo / 2)] with <= kMaxSteps pencil steps and the
+// least modelled cost (a power-of-16 length often beats the shortest one);
+// else the shortest such length up to min(lmax, 4 lo + 64); -1 if none.
+int fft_bluestein_len(int lo, std::vector<int>& radices, int lmax) {
+  std::vector<int> primes, rad;
+  int best = -1;
+  int64_t best_cost = 0;
+  for (int cand = lo; cand <= std::min(lmax, lo + lo / 2); ++cand)
+    if (factor_primes(cand, 13, primes)) {
+      group_pencils(primes, rad);
+      if ((int)rad.size() > kMaxSteps) continue;
+      const int64_t c = bluestein_cost(cand, rad);
+      if (best < 0 || c < best_cost) {
+        best = cand;
+        best_cost = c;
+        radices = rad;
+      }
+    }
+  if (best > 0) return best;
+  for (int cand = lo; cand <= std::min(lmax, 4 * lo + 64); ++cand)
     if (factor_primes(cand, 13, primes)) {
       group_pencils(primes, radices);
       if ((int)radices.size() <= kMaxSteps) return cand;
@@ -617,7 +653,10 @@ int fft_plan_ring(int n, RingPlan& rp, int mcap) {
     // spans n + 2 mcap lags (the chirp is n-periodic for even n), not 2n - 1.
     const bool pruned = mcap >= 0 && n % 2 == 0 && n + 2 * mcap < 2 * n - 1;
     std::vector<int> rad;
-    const int L = fft_bluestein_len(pruned ? n + 2 * mcap : 2 * n - 1, rad);
+    // prefer lengths that keep two CTAs per SM (<= 6022 points in 100 KB)
+    const int lo = pruned ? n + 2 * mcap : 2 * n - 1;
+    int L = fft_bluestein_len(lo, rad, kWholeBluesteinPair);
+    if (L < 0) L = fft_bluestein_len(lo, rad, kWholeBluesteinMax);
     if (L > 0 && L <= kWholeBluesteinMax) {
       rp.ring_blue = true;
       rp.L = L;
@@ -638,7 +677,7 @@ int fft_plan_ring(int n, RingPlan& rp, int mcap) {
   for (int p : big) {
     rp.radices.push_back(p);  // factor-local Bluestein steps last (contiguous pencils)
     std::vector<int> inner;
-    const int Lp = fft_bluestein_len(2 * p - 1, inner);
+    const int Lp = fft_bluestein_len(2 * p - 1, inner, kFftMaxLen);
     if (Lp < 0) return SHT_ERR_CONFIG;
     maxLp = std::max(maxLp, Lp);
   }
@@ -748,7 +787,7 @@ int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps
     FftStep& st = ring[j];
     if (st.R <= 31) continue;
     std::vector<int> irad;
-    const int Lp = fft_bluestein_len(2 * st.R - 1, irad);
+    const int Lp = fft_bluestein_len(2 * st.R - 1, irad, kFftMaxLen);
     const int base = (int)((int64_t)arena.size() - tw_off);
     push_table(arena, Lp);
     st.blue = 1;

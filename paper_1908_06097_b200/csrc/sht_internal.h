@@ -169,6 +169,7 @@ struct RingPlan {
   int wlen = 0;                // factor-local Bluestein: work buffer per pencil (Lp)
 };
 constexpr int kWholeBluesteinMax = 6912;   // longest whole-ring Bluestein transform
+constexpr int kWholeBluesteinPair = 6022;  // longest one whose buffer fits 100 KB (two CTAs per SM)
 // mcap >= 0: the transform only needs / only feeds the wavenumbers |k| <= mcap
 int fft_plan_ring(int n, RingPlan& rp, int mcap = -1);
 // Appends the ring's steps (and inner steps) to `steps`, its tables to `arena`.
@@ -179,6 +180,6 @@ int fft_pos(int k, const std::vector<int>& radices);
 // Shared-memory complex slots for n FFT points (one pad slot per 16 against bank conflicts).
 __host__ __device__ inline size_t fft_slots(size_t n) { return n + n / 16 + 1; }
 // Smallest 13-smooth length >= lo whose pencil plan has <= kMaxSteps steps.
-int fft_bluestein_len(int lo, std::vector<int>& radices);
+int fft_bluestein_len(int lo, std::vector<int>& radices, int lmax);
 
 }  // namespace sht
