@@ -88,18 +88,20 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50", "-i", str(gpu_index)], stdout=self.f,
+                                       "-lms", "100", "-i", str(gpu_index)], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
-        # do not open the timed region before the sampler is live
+        self.skip = 0
+        # NVML start-up must be over before the timed region: wait for the first samples
         t0 = time.perf_counter()
         while self.p is not None and time.perf_counter() - t0 < 5.0:
-            self.f.flush()
             if Path(self.f.name).stat().st_size > 0:
                 break
             time.sleep(0.01)
-        self.f.seek(0, os.SEEK_END)
+
+    def mark(self) -> None:
+        """Start of the timed region: later samples are the ones that count."""
         self.skip = Path(self.f.name).stat().st_size
 
     def stop(self) -> dict | None:
@@ -256,13 +258,15 @@ def run_ours(args):
         sh.inv_trans(spec, out=grid)
         sh.dir_trans(grid, out=spec2)
 
+    clk = Clocks(local) if rank == 0 else None  # started before the warm-up (NVML start-up)
     for _ in range(args.warmup):
         pair()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = Clocks(local) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.mark()
     e0.record()
     for _ in range(args.steps):
         pair()
