@@ -108,6 +108,26 @@ def test_size_matrix_golden(lib):
         assert ms["rotated_concurrent"] <= min(ms.values()) + 1e-12   # the paper's winner
 
 
+def test_bluestein_length_matches_restatement(lib):
+    """libsht's cost-chosen whole-ring Bluestein lengths == the restatement used by the partition model."""
+    from oracle.transposition import _bluestein_len, _factor
+    from paper_1908_06097_b200 import fft_plan_info
+
+    checked = 0
+    for n in range(20, 2600, 4):
+        info = fft_plan_info(n)            # no pruning: |k| <= n/2 kept
+        primes, _ = _factor(n, n)
+        if not any(p > 31 for p in primes):
+            continue
+        L, rad = _bluestein_len(2 * n - 1, 6022)
+        if L < 0:
+            L, rad = _bluestein_len(2 * n - 1, 6912)
+        if 0 < L <= 6912:
+            assert info["length"] == L and info["radices"] == rad, n
+            checked += 1
+    assert checked > 100
+
+
 def test_fft_plans(lib):
     from paper_1908_06097_b200 import fft_plan_info
 
