@@ -455,18 +455,31 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       static_assert(NT == 256, "ChirpWalk strides by 256");
       const double sg = (N & 1) ? -1.0 : 1.0;
       ChirpWalk cw(chirp, N, threadIdx.x);
-      for (int m = threadIdx.x; m <= M; m += NT) {
-        double2 S = make_double2(0.0, 0.0), A = S;
-        if (!(p.debug & 2)) ld_slot(p.rows_in[rg.yrow_off + m] + (int64_t)fb * 4, S.x, S.y, A.x, A.y);
-        double2 fn = cadd(S, A), fs = csub(S, A);
-        if (m == 0) {
-          fn.y = 0.0;
-          fs.y = 0.0;
+      constexpr int U = 3;  // all of a thread's row loads in flight at once (M + 1 <= 768 in one round)
+      for (int m0 = threadIdx.x; m0 <= M; m0 += U * NT) {
+        double2 S[U], A[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int m = m0 + u * NT;
+          S[u] = A[u] = make_double2(0.0, 0.0);
+          if (m <= M && !(p.debug & 2))
+            ld_slot(p.rows_in[rg.yrow_off + m] + (int64_t)fb * 4, S[u].x, S[u].y, A[u].x, A[u].y);
         }
-        const double2 lo = cmul(make_double2(fn.x - fs.y, -(fn.y + fs.x)), cw.c);
-        buf[px(m)] = lo;
-        if (m) buf[px(N - m + rg.shift)] = cmul(make_double2(fn.x + fs.y, fn.y - fs.x), make_double2(sg * cw.c.x, sg * cw.c.y));
-        cw.step();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int m = m0 + u * NT;
+          if (m > M) break;
+          double2 fn = cadd(S[u], A[u]), fs = csub(S[u], A[u]);
+          if (m == 0) {
+            fn.y = 0.0;
+            fs.y = 0.0;
+          }
+          buf[px(m)] = cmul(make_double2(fn.x - fs.y, -(fn.y + fs.x)), cw.c);
+          if (m)
+            buf[px(N - m + rg.shift)] =
+                cmul(make_double2(fn.x + fs.y, fn.y - fs.x), make_double2(sg * cw.c.x, sg * cw.c.y));
+          cw.step();
+        }
       }
     } else
     #pragma unroll 4
