@@ -115,12 +115,13 @@ class Clocks:
         if not rows:  # a timed region shorter than the sampling period: the sample that bracketed it
             rows = [r.split(",") for r in txt.splitlines() if r.strip()][-1:]
         os.unlink(self.f.name)
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
+                pw.append(float(r[3]))
                 for k, nm in enumerate(names):
                     if r[4 + k].strip().lower() == "active":
                         reasons.add(nm)
@@ -128,7 +129,8 @@ class Clocks:
                 continue
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": float(np.mean(pw)) if pw else None}
 
 
 def dist_setup():
@@ -375,6 +377,11 @@ def run_ours(args):
             "setup_s": setup_s,
             "cpu_baseline": cpu,
             "clocks": clocks,
+            # SURVEY.md 8f row 3 (energy.py:83-119 energy_per_step): NVML board power of rank 0's GPU
+            # during the timed region x ms per pair, times the GPU count for the job
+            "energy": ({"j_per_pair": clocks["power_w"] * ms * 1e-3 * world, "avg_power_w_per_gpu": clocks["power_w"],
+                        "basis": "rank-0 GPU NVML power.draw mean over the timed region x n_gpus"}
+                       if clocks and clocks.get("power_w") else None),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
