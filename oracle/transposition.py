@@ -100,8 +100,8 @@ def ring_fft_cost(n: int, mcap: int) -> int:
         lo = n + 2 * mcap if pruned else 2 * n - 1
         L, rad = _bluestein_len(lo, 6022)
         if L < 0:
-            L, rad = _bluestein_len(lo, 6912)
-        if 0 < L <= 6912:
+            L, rad = _bluestein_len(lo, 12288)
+        if 0 < L <= 12288:
             return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
     rad = _pencils([p for p in primes if p <= 31]) + big
     if not rad:

@@ -168,7 +168,7 @@ struct RingPlan {
   std::vector<int> radices;    // steps (factor-local Bluestein primes last)
   int wlen = 0;                // factor-local Bluestein: work buffer per pencil (Lp)
 };
-constexpr int kWholeBluesteinMax = 6912;   // longest whole-ring Bluestein transform
+constexpr int kWholeBluesteinMax = 12288;  // longest whole-ring Bluestein transform (212 KB class: 1 CTA per SM)
 constexpr int kWholeBluesteinPair = 6022;  // longest one whose buffer fits 100 KB (two CTAs per SM)
 // mcap >= 0: the transform only needs / only feeds the wavenumbers |k| <= mcap
 int fft_plan_ring(int n, RingPlan& rp, int mcap = -1);

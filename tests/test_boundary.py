@@ -121,8 +121,8 @@ def test_bluestein_length_matches_restatement(lib):
             continue
         L, rad = _bluestein_len(2 * n - 1, 6022)
         if L < 0:
-            L, rad = _bluestein_len(2 * n - 1, 6912)
-        if 0 < L <= 6912:
+            L, rad = _bluestein_len(2 * n - 1, 12288)
+        if 0 < L <= 12288:
             assert info["length"] == L and info["radices"] == rad, n
             checked += 1
     assert checked > 100
@@ -138,7 +138,8 @@ def test_fft_plans(lib):
     big = fft_plan_info(2572)                                       # 4 * 643: whole-ring Bluestein
     assert big["bluestein"] and big["length"] >= 2 * 2572 - 1
     assert fft_plan_info(8016)["radices"][-1] == 167                # factor-local Bluestein step (TCo1999)
-    assert fft_plan_info(5476)["radices"][-2:] == [37, 37]          # two Bluestein steps (TCo1999 ring)
+    assert fft_plan_info(6364)["radices"][-2:] == [37, 43]          # two Bluestein steps (TCo1999 ring)
+    assert fft_plan_info(5476)["length"] == 11264                   # 4 * 37^2: whole-ring Bluestein, 212 KB class
     for n in list(range(20, 2600, 4)) + list(range(2600, 8020, 52)):   # TCo639 .. TCo1999 rings
         info = fft_plan_info(n)
         assert int(np.prod(info["radices"])) == info["length"]
