@@ -444,10 +444,15 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     const int nseq = min(rg.nb, rs.wk.f1 - fb);
     // zero the bins no coefficient reaches: (M, N - M + shift) and [N + shift, L)
     const int gap = L - 2 * M - 1, gap1 = N - 2 * M - 1 + rg.shift;
-    for (int idx = threadIdx.x; idx < nseq * gap; idx += NT) {
-      const int q = idx / gap, g = idx - q * gap;
-      const int k = g < gap1 ? M + 1 + g : N + rg.shift + (g - gap1);
-      buf[px(q * L + k)] = make_double2(0.0, 0.0);
+    if (nseq == 1) {  // two plain ranges, no division
+      for (int k = M + 1 + threadIdx.x; k <= M + gap1; k += NT) buf[px(k)] = make_double2(0.0, 0.0);
+      for (int k = N + rg.shift + threadIdx.x; k < L; k += NT) buf[px(k)] = make_double2(0.0, 0.0);
+    } else {
+      for (int idx = threadIdx.x; idx < nseq * gap; idx += NT) {
+        const int q = idx / gap, g = idx - q * gap;
+        const int k = g < gap1 ? M + 1 + g : N + rg.shift + (g - gap1);
+        buf[px(q * L + k)] = make_double2(0.0, 0.0);
+      }
     }
     // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
     // (one thread per (m, field): a row's 32-byte field slots are read once)
