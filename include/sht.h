@@ -49,7 +49,8 @@ extern "C" {
 #define SHT_ERR_COMM 3
 
 /* plan flags */
-#define SHT_FLAG_RECOMPUTE_LEGENDRE 1 /* no P table: polynomials recomputed inside the Legendre GEMMs */
+#define SHT_FLAG_RECOMPUTE_LEGENDRE 1 /* no stored P table: the polynomials are regenerated on the GPU every
+                                       * transform (see the Legendre notes in DESIGN.md section 4) */
 #define SHT_FLAG_PROFILE_PHASES 2     /* record CUDA events around every phase (sht_phase_ms) */
 
 typedef struct sht_plan sht_plan;
@@ -112,9 +113,26 @@ int sht_transport(const sht_plan* plan, int* p2p);
 /* 128-byte NCCL unique id (call on rank 0 only). */
 int sht_nccl_get_unique_id(void* out128);
 
-/* Collective when nranks > 1 (a barrier over the plan's communicator before
- * the peer mappings are released). */
+/* Local release of the plan (no collective).  When nranks > 1 call
+ * sht_plan_close instead, unless a peer has failed: a peer may still store
+ * into this rank's receive buffers until it has passed close's barrier. */
 void sht_plan_destroy(sht_plan* plan);
+
+/* Collective teardown (nranks > 1): a barrier over the plan's communicator,
+ * bounded by SHT_COMM_TIMEOUT_MS, then sht_plan_destroy.  Returns
+ * SHT_ERR_COMM if a peer did not arrive (the plan is released either way).
+ * Replaces nothing in the reference; its analogue is the router's
+ * first-error abort (halo/router.py:124-126, 199-205). */
+int sht_plan_close(sht_plan* plan);
+
+/* Waits for `cuda_stream` (all transforms enqueued on it) with failure
+ * detection: polls the stream, the p2p handshake error word (a handshake
+ * waits at most SHT_COMM_TIMEOUT_MS, default 60000, for a peer) and NCCL's
+ * asynchronous error.  timeout_ms <= 0 uses SHT_COMM_TIMEOUT_MS.  Returns
+ * SHT_ERR_COMM (-> ProtocolError) if a peer failed or the wait timed out; the
+ * communicator is then aborted.  Every sht_inv_trans / sht_dir_trans also
+ * returns SHT_ERR_COMM once a handshake of the plan has timed out. */
+int sht_wait(sht_plan* plan, void* cuda_stream, int timeout_ms);
 
 const char* sht_last_error(void);
 

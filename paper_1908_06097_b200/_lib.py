@@ -25,7 +25,7 @@ SHT_FLAG_PROFILE_PHASES = 2
 # every symbol include/sht.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "sht_version", "sht_plan_create", "sht_inv_trans", "sht_dir_trans", "sht_local_layout",
-    "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_transport", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_last_error",
+    "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_transport", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_plan_close", "sht_wait", "sht_last_error",
     "sht_plan_validate", "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
 )
 
@@ -63,6 +63,8 @@ def load() -> C.CDLL:
     lib.sht_nccl_get_unique_id.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.argtypes = [C.c_void_p]
     lib.sht_plan_destroy.restype = None
+    lib.sht_plan_close.argtypes = [C.c_void_p]
+    lib.sht_wait.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     lib.sht_plan_validate.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int]
     lib.sht_gauss_nodes.argtypes = [C.c_int, f64p, f64p, f64p]
     lib.sht_partition.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i32p, i32p]

@@ -480,19 +480,25 @@ size_t leg_inv_smem() { return (size_t)kStages * kInvStageDbl * sizeof(double); 
 size_t leg_dir_smem() { return (size_t)kStages * kDirStageDbl * sizeof(double); }
 
 void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: set it once for every device a plan runs on
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !(done >> dev & 1)) {
     cudaFuncSetAttribute(leg_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
-    attr = true;
+    if (dev < 64) done |= 1ull << dev;
   }
   leg_inv_kernel<<<grid, kLegThreads, leg_inv_smem(), s>>>(p, spec, four);
 }
 
 void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: set it once for every device a plan runs on
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !(done >> dev & 1)) {
     cudaFuncSetAttribute(leg_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_dir_smem());
-    attr = true;
+    if (dev < 64) done |= 1ull << dev;
   }
   leg_dir_kernel<<<grid, kLegThreads, leg_dir_smem(), s>>>(p, four, spec);
 }

@@ -15,6 +15,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -236,21 +238,24 @@ struct sht_plan {
   double** d_ring_out = nullptr;                // [nh] leg_inv destination row of (ring, lm = 0)
   double** d_rows_out = nullptr;                // fft_g2f destination row per (local ring, m)
   const double** d_rows_in = nullptr;           // fft_f2g source row per (local ring, m)
+  // failure detection (nranks > 1): handshake error word in mapped host memory
+  int32_t* h_err = nullptr;
+  int32_t* d_err = nullptr;
+  uint64_t timeout_ns = 60ull * 1000000000ull;  // SHT_COMM_TIMEOUT_MS (default 60 s)
+  bool failed = false;                          // an error was reported: no collective teardown
+  std::string fail_msg;
 };
 
 namespace sht {
 
+// Local release of a plan (sht_plan_destroy): no collective.  With the p2p
+// transport a peer may still store into this rank's buffers until it has
+// passed the collective barrier of sht_plan_close, which a well-behaved
+// caller runs first; without it the device is synchronised (this rank's own
+// kernels are done) and the buffers are released.
 static void free_plan(sht_plan* p) {
   if (!p) return;
-  if (p->p2p && p->comm) {  // no peer may still store into our buffers or flags
-    cudaDeviceSynchronize();
-    int* d = nullptr;
-    if (cudaMalloc((void**)&d, sizeof(int)) == cudaSuccess) {
-      ncclAllReduce(d, d, 1, ncclInt, ncclSum, p->comm, 0);
-      cudaStreamSynchronize(0);
-      cudaFree(d);
-    }
-  }
+  if (p->nranks > 1) cudaDeviceSynchronize();
   for (int d = 0; d < (int)p->peer_x.size(); ++d) {
     if (d == p->rank) continue;
     if (p->peer_x[d]) cudaIpcCloseMemHandle(p->peer_x[d]);
@@ -268,7 +273,13 @@ static void free_plan(sht_plan* p) {
     for (auto& set : p->hist)
       for (auto& e : set) cudaEventDestroy(e);
   }
-  if (p->comm) ncclCommDestroy(p->comm);
+  if (p->h_err) cudaFreeHost(p->h_err);
+  if (p->comm) {
+    if (p->failed)
+      ncclCommAbort(p->comm);  // a peer is gone: destroy would wait for it
+    else
+      ncclCommDestroy(p->comm);
+  }
   delete p;
 }
 
@@ -298,6 +309,11 @@ static int64_t ring_fft_cost(int n, int mcap) {
 // ring pairs left one rank ~12% more FFT time at P = 2.
 static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, std::vector<int>& ring_owner) {
   if (P < 1) return fail(SHT_ERR_CONFIG, "nranks must be >= 1");
+  // every rank must own at least one wavenumber and one ring pair, or its
+  // local arrays are empty while its peers wait for it in the handshakes
+  if (P > g.T + 1 || P > g.nh)
+    return fail(SHT_ERR_CONFIG, "nranks (" + std::to_string(P) + ") exceeds min(truncation + 1, ndgl / 2) = " +
+                                    std::to_string(std::min(g.T + 1, g.nh)));
   snake(g.T + 1, P, m_owner);
   std::vector<int64_t> cost(g.nh);
   std::vector<int> order(g.nh);
@@ -325,11 +341,24 @@ enum FlagSlot { kYArr = 0, kXArr = 1, kYFree = 2, kXFree = 3 };
 // `sig_v` in slot `sig_slot` of peer t's flag words (release, system scope:
 // orders every store this GPU made before it in stream order, including the
 // previous kernel's NVLink stores), then wait until peer t has published at
-// least `wait_v` in slot `wait_slot` of ours (acquire).
+// least `wait_v` in slot `wait_slot` of ours (acquire).  The wait is bounded:
+// after `timeout_ns` (SHT_COMM_TIMEOUT_MS) without the peer's flag the
+// kernel records (peer + 1, slot) in the host-mapped error word and returns,
+// and every later handshake of the plan returns at once, so a dead or
+// desynchronised peer turns into SHT_ERR_COMM on the host instead of a hang
+// (the reference's first-error abort, halo/router.py:124-126, 199-205).
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void flag_kernel(uint32_t* const* peer_flags, const uint32_t* flags, int P, int r, int sig_slot,
-                            uint32_t sig_v, int wait_slot, uint32_t wait_v) {
+                            uint32_t sig_v, int wait_slot, uint32_t wait_v, uint64_t timeout_ns,
+                            volatile int32_t* err) {
   const int t = threadIdx.x;
   if (t >= P || t == r) return;
+  if (err[0] != 0) return;  // the plan already failed: drain the stream
   if (sig_slot >= 0) {
     __threadfence_system();
     uint32_t* a = peer_flags[t] + sig_slot * P + r;
@@ -337,10 +366,19 @@ __global__ void flag_kernel(uint32_t* const* peer_flags, const uint32_t* flags, 
   }
   if (wait_slot >= 0) {
     const uint32_t* a = flags + wait_slot * P + t;
-    for (;;) {
+    const uint64_t t0 = globaltimer_ns();
+    for (int it = 0;; ++it) {
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
       if ((int32_t)(v - wait_v) >= 0) break;
+      if ((it & 63) == 63) {
+        if (err[0] != 0) return;
+        if (globaltimer_ns() - t0 > timeout_ns) {
+          atomicCAS((int32_t*)err, 0, (t + 1) * 16 + wait_slot);
+          __threadfence_system();
+          return;
+        }
+      }
       __nanosleep(128);
     }
   }
@@ -348,9 +386,82 @@ __global__ void flag_kernel(uint32_t* const* peer_flags, const uint32_t* flags, 
 
 static int flags_op(sht_plan* p, int sig_slot, uint32_t sig_v, int wait_slot, uint32_t wait_v, cudaStream_t s) {
   flag_kernel<<<1, 32 * ((p->nranks + 31) / 32), 0, s>>>(p->d_peer_flags, p->flagw, p->nranks, p->rank, sig_slot,
-                                                          sig_v, wait_slot, wait_v);
+                                                          sig_v, wait_slot, wait_v, p->timeout_ns, p->d_err);
   SHT_CUDA_TRY(cudaGetLastError());
   return SHT_OK;
+}
+
+// Host-side view of the plan's communication health: the handshake error
+// word (written by flag_kernel) and NCCL's asynchronous error state.
+static int comm_check(sht_plan* p) {
+  if (p->failed) return fail(SHT_ERR_COMM, "the plan failed earlier (" + p->fail_msg + "); close it");
+  if (p->h_err && p->h_err[0] != 0) {
+    const int v = p->h_err[0];
+    static const char* slot[] = {"rows-arrived (inverse)", "rows-arrived (direct)", "buffer-drained (inverse)",
+                                 "buffer-drained (direct)"};
+    return fail(SHT_ERR_COMM, "transposition handshake timed out after " + std::to_string(p->timeout_ns / 1000000) +
+                                  " ms waiting for rank " + std::to_string(v / 16 - 1) + " (" + slot[(v % 16) & 3] +
+                                  "); the peer is dead or desynchronised");
+  }
+  if (p->comm) {
+    ncclResult_t st = ncclSuccess;
+    if (ncclCommGetAsyncError(p->comm, &st) == ncclSuccess && st != ncclSuccess && st != ncclInProgress)
+      return fail(SHT_ERR_COMM, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st));
+  }
+  return SHT_OK;
+}
+
+// Waits for stream `s` with a bound: polls the stream, the handshake error
+// word and NCCL's asynchronous error; on a peer failure or after
+// `timeout_ns` the plan is marked failed (its NCCL communicator is aborted at
+// destroy, so no later collective waits for the dead peer).
+static int wait_stream(sht_plan* p, cudaStream_t s, uint64_t timeout_ns) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(SHT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+    if (int rc = comm_check(p)) {
+      p->failed = true;
+      p->fail_msg = g_err;
+      if (p->comm) ncclCommAbort(p->comm), p->comm = nullptr;
+      return rc;
+    }
+    const uint64_t el = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            std::chrono::steady_clock::now() - t0).count();
+    if (el > timeout_ns) {
+      p->failed = true;
+      if (p->comm) ncclCommAbort(p->comm), p->comm = nullptr;
+      p->fail_msg = "transform did not complete within " + std::to_string(timeout_ns / 1000000) +
+                    " ms (a peer is dead or desynchronised); communicator aborted";
+      return fail(SHT_ERR_COMM, p->fail_msg);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  if (int rc = comm_check(p)) {
+    p->failed = true;
+    p->fail_msg = g_err;
+    return rc;
+  }
+  return SHT_OK;
+}
+
+// Collective teardown barrier (sht_plan_close): after it no peer stores into
+// this rank's buffers any more.
+static int close_barrier(sht_plan* p) {
+  if (p->nranks < 2 || !p->comm || p->failed) return SHT_OK;
+  SHT_CUDA_TRY(cudaDeviceSynchronize());
+  cudaStream_t s;
+  SHT_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int* d = nullptr;
+  int rc = SHT_OK;
+  if (cudaMalloc((void**)&d, sizeof(int)) != cudaSuccess) rc = fail(SHT_ERR_CUDA, "cudaMalloc (close barrier)");
+  if (!rc && ncclAllReduce(d, d, 1, ncclInt, ncclSum, p->comm, s) != ncclSuccess)
+    rc = fail(SHT_ERR_COMM, "ncclAllReduce (close barrier)");
+  if (!rc) rc = wait_stream(p, s, p->timeout_ns);
+  if (d) cudaFree(d);
+  cudaStreamDestroy(s);
+  return rc;
 }
 
 // Chooses the transport and builds the row-pointer tables the kernels store
@@ -371,6 +482,9 @@ static int build_transport(sht_plan* p) {
     SHT_CUDA_TRY(cudaMalloc((void**)&p->flagw, 4 * P * sizeof(uint32_t)));
     SHT_CUDA_TRY(cudaMemset(p->flagw, 0, 4 * P * sizeof(uint32_t)));
     p->peer_flags[r] = p->flagw;
+    SHT_CUDA_TRY(cudaHostAlloc((void**)&p->h_err, 4 * sizeof(int32_t), cudaHostAllocMapped));
+    std::memset(p->h_err, 0, 4 * sizeof(int32_t));
+    SHT_CUDA_TRY(cudaHostGetDevicePointer((void**)&p->d_err, p->h_err, 0));
     struct Rec {
       int32_t ok[16];
       cudaIpcMemHandle_t h[3];
@@ -931,6 +1045,8 @@ static sht_plan* new_plan(int nfld, int rank, int nranks, int flags) {
   p->flags = flags;
   if (const char* dbg = getenv("SHT_FFT_DEBUG")) p->fft_debug = atoi(dbg);
   if (const char* dbg = getenv("SHT_LEG_DEBUG")) p->leg_debug = atoi(dbg);
+  if (const char* to = getenv("SHT_COMM_TIMEOUT_MS"))
+    p->timeout_ns = (uint64_t)std::max(1LL, atoll(to)) * 1000000ull;
   return p;
 }
 
@@ -954,6 +1070,21 @@ int sht_plan_create(int truncation, int ndgl, const int32_t* nloen, int nfld, in
 }
 
 void sht_plan_destroy(sht_plan* plan) { free_plan(plan); }
+
+int sht_plan_close(sht_plan* plan) {
+  if (!plan) return SHT_OK;
+  const int rc = close_barrier(plan);
+  const std::string msg = g_err;
+  free_plan(plan);
+  g_err = msg;
+  return rc;
+}
+
+int sht_wait(sht_plan* plan, void* stream, int timeout_ms) {
+  if (!plan) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  const uint64_t to = timeout_ms > 0 ? (uint64_t)timeout_ms * 1000000ull : plan->timeout_ns;
+  return wait_stream(plan, (cudaStream_t)stream, to);
+}
 
 int sht_local_layout(const sht_plan* p, int64_t* nspec_re, int64_t* npts, int32_t* m_list, int32_t* n_m,
                      int32_t* ring_list, int32_t* n_rings) {
@@ -1068,6 +1199,7 @@ int sht_inv_trans(sht_plan* p, const double* spec, double* grid, void* stream) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   if (int rc = check_ptr(spec, "spec")) return rc;
   if (int rc = check_ptr(grid, "grid")) return rc;
+  if (int rc = comm_check(p)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t e = ++p->inv_epoch;
   if (p->p2p)
@@ -1085,6 +1217,7 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
   if (int rc = check_ptr(spec, "spec")) return rc;
   if (int rc = check_ptr(grid, "grid")) return rc;
+  if (int rc = comm_check(p)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t e = ++p->dir_epoch;
   if (p->p2p)

@@ -158,8 +158,11 @@ class SHTransform:
     def phase_ms(self, npairs: int = 1) -> dict:
         """Device times (ms) per phase, averaged over the last ``npairs`` (<= 64)
         inv_trans + dir_trans pairs (plan created with profile=True)."""
+        import torch
+
         v = (C.c_float * 7)()
-        _lib.check(self._lib.sht_phase_ms_avg(self._plan, int(npairs), v, 7))
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.sht_phase_ms_avg(self._plan, int(npairs), v, 7))
         keys = ("legendre_poly_setup", "inv_legendre", "inv_alltoall", "inv_fft", "dir_fft", "dir_alltoall",
                 "dir_legendre")
         return dict(zip(keys, [float(x) for x in v]))
@@ -183,22 +186,43 @@ class SHTransform:
     def _run(self, fn, x, ncols_in: int, ncols_out: int, out, stream):
         import torch
 
-        host = isinstance(x, np.ndarray)
-        if host:
-            xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
-            xt = xt.to(self.device, non_blocking=True)
-        else:
-            xt = x
-        self._check(xt, ncols_in, "input")
-        if out is None:
-            out = torch.empty((self.nfld, ncols_out), dtype=torch.float64, device=self.device)
-        else:
-            self._check(out, ncols_out, "out")
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _lib.check(fn(self._plan, C.c_void_p(xt.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
-        if host:
-            return out.cpu().numpy()
+        if getattr(self, "_plan", None) is None:
+            raise ConfigurationError("the plan is closed")
+        with torch.cuda.device(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream(self.device)
+            host = isinstance(x, np.ndarray)
+            if host:  # copy in on the transform's stream, so it is ordered before the kernels
+                xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
+                with torch.cuda.stream(s):
+                    xt = xt.to(self.device, non_blocking=True)
+            else:
+                xt = x
+            self._check(xt, ncols_in, "input")
+            if out is None:
+                with torch.cuda.stream(s):
+                    out = torch.empty((self.nfld, ncols_out), dtype=torch.float64, device=self.device)
+            else:
+                self._check(out, ncols_out, "out")
+            _lib.check(fn(self._plan, C.c_void_p(xt.data_ptr()), C.c_void_p(out.data_ptr()),
+                          C.c_void_p(s.cuda_stream)))
+            if host:  # bounded wait (peer failure -> ProtocolError), then the copy back on the same stream
+                self.synchronize(s)
+                with torch.cuda.stream(s):
+                    res = out.cpu()
+                return res.numpy()
         return out
+
+    def synchronize(self, stream=None, timeout_ms: int = 0) -> None:
+        """Wait for the transforms enqueued on ``stream`` (default: the current
+        stream) with failure detection: raises ``ProtocolError`` when a peer
+        rank died or desynchronised (handshake timeout, NCCL asynchronous
+        error) or the wait exceeded ``timeout_ms`` (<= 0: SHT_COMM_TIMEOUT_MS,
+        default 60 s)."""
+        import torch
+
+        with torch.cuda.device(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream(self.device)
+            _lib.check(self._lib.sht_wait(self._plan, C.c_void_p(s.cuda_stream), int(timeout_ms)))
 
     # ------------------------------------------------------------------ API
     def inv_trans(self, spec, out=None, stream=None):
@@ -222,6 +246,12 @@ class SHTransform:
         buffers), so PCIe in, PCIe out and the transform overlap.  Returns when
         the work is enqueued; the caller's current stream waits for every copy
         back (synchronize it before reading host_out)."""
+        import torch
+
+        with torch.cuda.device(self.device):
+            self._pairs_pipelined(host_in, host_out)
+
+    def _pairs_pipelined(self, host_in, host_out) -> None:
         import torch
 
         dev = self.device
@@ -257,14 +287,34 @@ class SHTransform:
         cs.wait_stream(P["d2h"])
 
     def close(self) -> None:
+        """Release the plan.  Collective when the plan spans several ranks (a
+        bounded barrier, so no peer still stores into this rank's buffers);
+        raises ``ProtocolError`` if a peer does not arrive."""
+        import torch
+
         self._pipe = None
-        if getattr(self, "_plan", None):
-            self._lib.sht_plan_destroy(self._plan)
-            self._plan = None
+        plan, self._plan = getattr(self, "_plan", None), None
+        if plan:
+            with torch.cuda.device(self.device):
+                _lib.check(self._lib.sht_plan_close(plan))
 
     def __del__(self):
+        # local release only: a collective in a destructor hangs every peer
+        # when one rank raised or never collects its plan
+        plan = getattr(self, "_plan", None)
+        if not plan:
+            return
+        self._plan = None
         try:
-            self.close()
+            if self.nranks > 1:
+                import warnings
+
+                warnings.warn("SHTransform spanning several ranks was not close()d; releasing it locally",
+                              ResourceWarning)
+            import torch
+
+            with torch.cuda.device(self.device):
+                self._lib.sht_plan_destroy(plan)
         except Exception:
             pass
 

@@ -1,5 +1,17 @@
-"""Multi-GPU parity: torchrun over 2 (or more) B200 with the NCCL
-transposition; every rank compares its local slice with the 1-rank oracle."""
+"""Multi-GPU parity and failure handling: torchrun over 2 / 4 B200.
+
+* parity: every rank compares its local slice of K >= 4 back-to-back
+  inverse + direct pairs (distinct inputs, no host sync in between) with the
+  1-rank oracle (tools/mp_check.py), for both transports of the
+  grid <-> spectral transposition -- p2p (kernels store into the peers'
+  buffers over NVLink, flag handshakes) and NCCL grouped send/recv in the
+  reference's rotated order (collectives.py:85-86) -- and for the recompute
+  Legendre mode;
+* failure: one rank dies after plan creation; the survivors must raise
+  ProtocolError from their bounded wait instead of hanging
+  (tools/mp_fail_check.py; the reference's first-error abort,
+  halo/router.py:124-126, 199-205).
+"""
 
 import os
 import subprocess
@@ -18,15 +30,33 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_torchrun_parity(nproc):
-    if _ngpu() < nproc:
-        pytest.skip(f"needs {nproc} GPUs")
+def _torchrun(nproc, script, args, env_extra, port, timeout=900):
+    env = dict(os.environ, **env_extra)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr=127.0.0.1", f"--master-port={29600 + nproc}", str(ROOT / "tools" / "mp_check.py"),
-           "79", "6", "319", "5", "639", "4"]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tools" / script), *args]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
     sys.stdout.write(res.stdout[-4000:])
     sys.stderr.write(res.stderr[-4000:])
+    return res
+
+
+@pytest.mark.parametrize("nproc,transport,recompute", [(2, "p2p", 0), (2, "nccl", 0), (2, "p2p", 1),
+                                                        (4, "p2p", 0), (4, "nccl", 0)])
+def test_torchrun_parity(nproc, transport, recompute):
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    port = 29600 + 10 * nproc + (transport == "nccl") + 2 * recompute
+    res = _torchrun(nproc, "mp_check.py", ["79", "6", "319", "5", "639", "4"],
+                    {"SHT_TRANSPORT": transport, "SHT_RECOMPUTE": str(recompute), "MP_PAIRS": "4"}, port)
     assert res.returncode == 0
     assert "MP_OK" in res.stdout
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_dead_peer_raises_protocol_error(transport):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _torchrun(2, "mp_fail_check.py", ["79", "4"],
+                    {"SHT_TRANSPORT": transport, "SHT_COMM_TIMEOUT_MS": "5000", "TORCH_NCCL_ASYNC_ERROR_HANDLING": "0"},
+                    29680 + (transport == "nccl"), timeout=300)
+    assert "FAIL_OK" in res.stdout, res.stdout[-2000:]
