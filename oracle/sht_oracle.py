@@ -196,16 +196,20 @@ def legendre_m(T: int, m: int, mu: np.ndarray, mant_mm: np.ndarray, expo_mm: np.
     return out
 
 
-def legendre_table(T: int, mu: np.ndarray, sint: np.ndarray, mcap_north: np.ndarray):
+def legendre_table(T: int, mu: np.ndarray, sint: np.ndarray, mcap_north: np.ndarray, m_subset=None):
     """All P_n^m on the northern rings that need them.
 
     Returns a list over m of (i0, P) where rings i0..NH-1 are the rings with
     M_i >= m (M is non-decreasing toward the equator) and P has shape
-    [NH - i0, T - m + 1].
+    [NH - i0, T - m + 1].  With ``m_subset`` only those wavenumbers get a
+    table (the others are None): a TCo1999 table is 27 GB, a few m are not.
     """
     mant, expo = legendre_diag(T, sint)
     tables = []
     for m in range(T + 1):
+        if m_subset is not None and m not in m_subset:
+            tables.append(None)
+            continue
         i0 = int(np.searchsorted(mcap_north, m, side="left"))
         tables.append((i0, legendre_m(T, m, mu[i0:], mant[m, i0:], expo[m, i0:])))
     return tables
@@ -252,7 +256,8 @@ class SHTransformOracle:
     (north first, north/south symmetric).
     """
 
-    def __init__(self, truncation: int, grid="octahedral", nfld: int = 1, workers: int | None = None):
+    def __init__(self, truncation: int, grid="octahedral", nfld: int = 1, workers: int | None = None,
+                 m_subset=None):
         T = int(truncation)
         self.workers = int(workers) if workers else (os.cpu_count() or 1)
         if T < 1:
@@ -276,7 +281,10 @@ class SHTransformOracle:
         self.roff = ring_offsets(nloen)
         self.npts = int(self.roff[-1])
         self.mu, self.sint, self.w = gauss_nodes(self.ndgl)
-        self.tables = legendre_table(T, self.mu, self.sint, self.mcap[: self.nh])
+        # m_subset: restrict the transform to these zonal wavenumbers (inv_trans
+        # ignores the other coefficients, dir_trans returns zeros for them)
+        self.m_subset = None if m_subset is None else {int(m) for m in m_subset}
+        self.tables = legendre_table(T, self.mu, self.sint, self.mcap[: self.nh], self.m_subset)
         self.soff = spec_offsets(T)
         self.nspec = nspec_real(T)
 
@@ -290,6 +298,8 @@ class SHTransformOracle:
         T, nh, nf = self.T, self.nh, self.nfld
         four = [np.zeros((nf, int(self.mcap[j]) + 1), dtype=np.complex128) for j in range(self.ndgl)]
         for m in range(T + 1):
+            if self.tables[m] is None:
+                continue
             i0, P = self.tables[m]
             if i0 >= nh:
                 continue
@@ -334,6 +344,8 @@ class SHTransformOracle:
         T, nh, nf = self.T, self.nh, self.nfld
         spec = np.zeros((nf, self.nspec))
         for m in range(T + 1):
+            if self.tables[m] is None:
+                continue
             i0, P = self.tables[m]
             if i0 >= nh:
                 continue

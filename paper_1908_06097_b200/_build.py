@@ -1,7 +1,9 @@
 """Build libsht.so (the C-ABI of include/sht.h) in-tree with nvcc for sm_100a.
 
-The shared library lands next to this file so it travels with the repo
-snapshot to the GPU box (gpurun) and is what ``_lib.load()`` opens.
+Each CUDA source compiles to its own object under build/ (in parallel, and
+only when it or a header changed), then nvcc links the shared library next to
+this file so it travels with the repo snapshot to the GPU box (gpurun) and is
+what ``_lib.load()`` opens.
 """
 
 from __future__ import annotations
@@ -9,13 +11,16 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsht.so"
+OBJ = ROOT / "build" / "obj"
 SOURCES = ["sht_plan.cu", "sht_legendre.cu", "sht_fft.cu"]
+HEADERS = ["sht_internal.h", "fft_codelets.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -31,30 +36,39 @@ def nvcc() -> str:
     return cand if Path(cand).exists() else "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    srcs = [CSRC / s for s in SOURCES]
-    deps = srcs + [CSRC / "sht_internal.h", ROOT / "include" / "sht.h"]
-    if not force and LIB.exists() and LIB.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
-        return LIB
-    inc, lib = nccl_paths()
-    cmd = [
-        nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-        "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-        f"-I{inc}", f"-I{ROOT / 'include'}",
-        *[str(s) for s in srcs],
-        f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}",
-        "-o", str(LIB) + ".tmp",
-    ]
+def _run(cmd: list[str], verbose: bool) -> None:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libsht.so")
+        raise RuntimeError("nvcc failed: " + " ".join(cmd[-3:]))
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    inc, lib = nccl_paths()
+    hdrs = [CSRC / h for h in HEADERS if (CSRC / h).exists()] + [ROOT / "include" / "sht.h"]
+    newest_hdr = max(h.stat().st_mtime for h in hdrs)
+    OBJ.mkdir(parents=True, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+             "-Xptxas", "-v" if verbose else "-O3", f"-I{inc}", f"-I{ROOT / 'include'}"]
+    jobs = []
+    for s in SOURCES:
+        src, obj = CSRC / s, OBJ / (Path(s).stem + ".o")
+        if force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, newest_hdr):
+            jobs.append([nvcc(), *flags, "-c", str(src), "-o", str(obj) + ".tmp"])
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), jobs))
+    for c in jobs:
+        os.replace(c[-1], c[-1][:-4])
+    objs = [OBJ / (Path(s).stem + ".o") for s in SOURCES]
+    if jobs or force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        _run([nvcc(), *ARCH, "-shared", *[str(o) for o in objs], f"-L{lib}", "-l:libnccl.so.2",
+              "-Xlinker", f"-rpath={lib}", "-o", str(LIB) + ".tmp"], verbose)
+        os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

@@ -60,93 +60,124 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
-constexpr int kLegThreads = 256;
-constexpr int kStages = 2;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised pipeline: warps 0..7 consume (DMMA), warp 8 produces (bulk
+// copies).  kStages shared-memory stages, each with a "full" barrier (the
+// producer's expect_tx arrival + the copies' transaction bytes) and an
+// "empty" barrier (one arrival per consumer warp), so no CTA-wide barrier sits
+// in the K loop and the copy issue is off the DMMA warps' path.  CTAs walk the
+// wavenumber-major tile list with a static stride (tile = blockIdx.x + k *
+// gridDim.x): the list starts with the largest K, so the interleave balances.
+constexpr int kConsumers = 8;
+constexpr int kLegThreads = 32 * (kConsumers + 1);
+constexpr int kMaxStages = 4;
+
+struct Pipe {
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
+};
+
+template <int kStages>
+__device__ __forceinline__ void pipe_init(Pipe& pp) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&pp.full[s], 1);
+      mbar_init(&pp.empty[s], kConsumers);
+    }
+    fence_mbar_init();
+  }
+}
 
 // ------------------------------------------------------------------ leg_inv
-constexpr int kInvPStr = kInvKc + 8;          // 72 doubles: rows of P tile (== 8 mod 16 -> no LDS.128 conflicts)
-constexpr int kInvSStr = 2 * kInvKc + 2;      // 130 doubles: field rows of the spectral tile (== 2 mod 16)
+// 2 stages of 64 wavenumbers: the 128 row copies of a stage are what the
+// TMA unit can issue under one stage's DMMA work (at 32 per stage it cannot)
+constexpr int kInvStages = 2;
+constexpr int kInvKcP = 64;                    // k-chunk (wavenumbers n) per stage
+constexpr int kInvPStr = kInvKcP + 8;          // 72 doubles: P rows (== 8 mod 16 -> no LDS.128 conflicts)
+constexpr int kInvSStr = 2 * kInvKcP + 2;      // 130 doubles: field rows of the spectral tile (== 2 mod 16)
 constexpr int kInvPDbl = kInvRings * kInvPStr;
 constexpr int kInvSDbl = kLegFields * kInvSStr;
 constexpr int kInvStageDbl = kInvPDbl + kInvSDbl;
 
 // Tile: rings r0..r0+63 (northern index) x fields f0..f0+63 of wavenumber lm.
-// Warp w: rings 32*(w&1).. , fields 16*(w>>1)..  -> 4 ring groups x 2 field groups
-// x {S.re, S.im, A.re, A.im} DMMA accumulators (64 doubles per thread).
-// Operands arrive by 1-D bulk copies (one per P-table row and per field row,
-// issued by warp 0) completing on a per-stage mbarrier; the next tile's first
-// stages are issued before the current tile's epilogue stores.
+// Consumer warp w: rings 32*(w&1).. , fields 16*(w>>1)..  -> 4 ring groups x 2
+// field groups x {S.re, S.im, A.re, A.im} DMMA accumulators (64 doubles per thread).
 struct InvTile {
   int lm, r0, f0, K, nk, kp, nrows, nf;
   const double* P;
   const double* S;
 };
 
+__device__ __forceinline__ InvTile inv_tile(const LegParams& p, const double* spec, int t) {
+  InvTile c;
+  const LegTile tile = p.tiles[t];
+  c.lm = tile.lm;
+  c.r0 = tile.r0;
+  c.f0 = tile.f0;
+  const int m = p.lm_m[c.lm];
+  c.kp = p.lm_kp[c.lm];
+  c.K = p.T - m + 1;
+  c.nk = (c.K + kInvKcP - 1) / kInvKcP;
+  c.nrows = min(kInvRings, p.nh - c.r0);
+  c.nf = min(kLegFields, p.nfld - c.f0);
+  c.P = p.ptab + p.lm_poff[c.lm] + (int64_t)(c.r0 - p.lm_i0[c.lm]) * c.kp;
+  c.S = spec + 2 * p.lm_soff[c.lm];
+  return c;
+}
+
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ int s_tile;
-  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) Pipe pp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp & 1, wf = warp >> 1;
-  const int lr = lane >> 2, lc = lane & 3;
 
   // stale operand slots must hold finite values (they meet zero P padding or
   // feed discarded accumulator rows)
-  for (int i = tid; i < kStages * kInvStageDbl; i += kLegThreads) sm[i] = 0.0;
-  if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
-    fence_mbar_init();
-  }
+  for (int i = tid; i < kInvStages * kInvStageDbl; i += kLegThreads) sm[i] = 0.0;
+  pipe_init<kInvStages>(pp);
   fence_async_smem();
   __syncthreads();
 
-  auto make = [&](int t) {
-    InvTile c;
-    const LegTile tile = p.tiles[t];
-    c.lm = tile.lm;
-    c.r0 = tile.r0;
-    c.f0 = tile.f0;
-    const int m = p.lm_m[c.lm];
-    c.kp = p.lm_kp[c.lm];
-    c.K = p.T - m + 1;
-    c.nk = (c.K + kInvKc - 1) / kInvKc;
-    c.nrows = min(kInvRings, p.nh - c.r0);
-    c.nf = min(kLegFields, p.nfld - c.f0);
-    c.P = p.ptab + p.lm_poff[c.lm] + (int64_t)(c.r0 - p.lm_i0[c.lm]) * c.kp;
-    c.S = spec + 2 * p.lm_soff[c.lm];
-    return c;
-  };
-  // the bulk copies of k-chunk kc into stage st: one per P row and per field
-  // row, spread over all threads (the tx count may run ahead of expect_tx)
-  auto issue = [&](const InvTile& c, int kc, int st) {
-    if (p.debug & 1) return;
-    double* Ps = sm + st * kInvStageDbl;
-    double* Ss = Ps + kInvPDbl;
-    const int kcount = min(kInvKc, c.K - kc * kInvKc);
-    if (tid == 0) mbar_expect_tx(&full[st], (unsigned)(c.nrows * kInvKc * 8 + c.nf * kcount * 16));
-    for (int j = tid; j < c.nrows + c.nf; j += kLegThreads) {
-      if (j < c.nrows)
-        bulk_g2s(Ps + j * kInvPStr, c.P + (int64_t)j * c.kp + kc * kInvKc, kInvKc * 8, &full[st]);
-      else {
-        const int f = j - c.nrows;
-        bulk_g2s(Ss + f * kInvSStr, c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kc * kInvKc, kcount * 16,
-                 &full[st]);
+  if (warp == kConsumers) {  // ---- producer: one bulk copy per P row / field row and k-chunk
+    int st = 0;
+    unsigned ph = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const InvTile c = inv_tile(p, spec, t);
+      for (int kc = 0; kc < c.nk; ++kc) {
+        mbar_wait(&pp.empty[st], ph ^ 1);
+        double* Ps = sm + st * kInvStageDbl;
+        double* Ss = Ps + kInvPDbl;
+        const int kcount = min(kInvKcP, c.K - kc * kInvKcP);
+        if (lane == 0) mbar_expect_tx(&pp.full[st], (unsigned)(c.nrows * kInvKcP * 8 + c.nf * kcount * 16));
+        __syncwarp();
+        for (int j = lane; j < c.nrows + c.nf; j += 32) {
+          if (j < c.nrows)
+            bulk_g2s(Ps + j * kInvPStr, c.P + (int64_t)j * c.kp + kc * kInvKcP, kInvKcP * 8, &pp.full[st]);
+          else {
+            const int f = j - c.nrows;
+            bulk_g2s(Ss + f * kInvSStr, c.S + (int64_t)(c.f0 + f) * p.spec_ld + 2 * kc * kInvKcP, kcount * 16,
+                     &pp.full[st]);
+          }
+        }
+        if (++st == kInvStages) {
+          st = 0;
+          ph ^= 1;
+        }
       }
     }
-  };
-  auto prologue = [&](const InvTile& c) {
-    for (int st = 0; st < kStages && st < c.nk; ++st) issue(c, st, st);
-  };
+    return;
+  }
 
-  unsigned phase = 0;  // bit st: parity of the next completion of full[st]
-  if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-  __syncthreads();
-  int t = s_tile;
-  if (t >= p.ntiles) return;
-  InvTile c = make(t);
-  prologue(c);
-  while (true) {
+  // ---- consumers
+  const int wr = warp & 1, wf = warp >> 1;
+  const int lr = lane >> 2, lc = lane & 3;
+  int st = 0;
+  unsigned ph = 0;
+  for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    const InvTile c = inv_tile(p, spec, t);
     double acc[4][2][4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g)
@@ -160,15 +191,13 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
-      const int st = kc & 1;
-      if (!(p.debug & 1)) mbar_wait(&full[st], (phase >> st) & 1);
-      phase ^= 1u << st;
-      if (active && !(p.debug & 2)) {
+      mbar_wait(&pp.full[st], ph);
+      if (active) {
         const double* Ps = sm + st * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
         const double* Ss = sm + st * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
-        const int smax = min(kInvKc / 8, (c.K - kc * kInvKc + 7) / 8);
+        const int smax = min(kInvKcP / 8, (c.K - kc * kInvKcP + 7) / 8);
 #pragma unroll
-        for (int sub = 0; sub < kInvKc / 8; ++sub) {
+        for (int sub = 0; sub < kInvKcP / 8; ++sub) {
           if (sub >= smax) break;
           double2 a[4], bs[2], ba[2];
 #pragma unroll
@@ -192,18 +221,16 @@ __global__ void __launch_bounds__(kLegThreads, 1)
             }
         }
       }
-      __syncthreads();  // stage st fully consumed
-      if (kc + kStages < c.nk) issue(c, kc + kStages, st);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pp.empty[st]);  // this warp is done with stage st
+      if (++st == kInvStages) {
+        st = 0;
+        ph ^= 1;
+      }
     }
-    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-    __syncthreads();
-    const int tn = s_tile;
-    InvTile cn;
-    if (tn < p.ntiles) {
-      cn = make(tn);
-      prologue(cn);  // next tile's operands stream in under this tile's stores
-    }
-
+    // epilogue: each (ring, field) slot as one 256-bit store straight into the
+    // ring owner's receive buffer (local, or a peer GPU over NVLink); the
+    // producer keeps filling the next tile's stages meanwhile
     if (active && !(p.debug & 4)) {
       const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
@@ -222,96 +249,100 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         }
       }
     }
-    if (tn >= p.ntiles) break;
-    c = cn;
-    __syncthreads();  // s_tile is rewritten at the end of the next tile
   }
 }
 
 // ------------------------------------------------------------------ leg_dir
+constexpr int kDirStages = 4;
+constexpr int kDirKcR = 16;                    // k-chunk (rings) per stage
 constexpr int kDirPStr = kDirN + 4;            // 132: P tile [ring][n]          (== 4 mod 16)
-constexpr int kDirBStr = 4 * kLegFields + 2;   // 258: B tile [ring][field][S.re, S.im, A.re, A.im]
-constexpr int kDirPDbl = kDirKc * kDirPStr;
-constexpr int kDirBDbl = kDirKc * kDirBStr;
+// B tile [ring][field][S.re, S.im, A.re, A.im]: row pitch a multiple of 128 B
+// plus a per-ring 16-byte offset {0, 1, 4, 5}[ring % 4], so the 8 lanes of an
+// LDS.128 phase (2 fields x 4 rings) hit 8 distinct bank groups
+constexpr int kDirBStr = 4 * kLegFields + 16;  // 272 doubles = 17 x 128 B
+__device__ __forceinline__ int dir_boff(int ring) { return 2 * ((ring & 1) + 4 * ((ring >> 1) & 1)); }
+constexpr int kDirPDbl = kDirKcR * kDirPStr;
+constexpr int kDirBDbl = kDirKcR * kDirBStr + 16;
 constexpr int kDirStageDbl = kDirPDbl + kDirBDbl;
 
 // Tile: n-m offsets n0..n0+127 (64 even-parity rows, 64 odd) x fields f0..f0+63.
-// Warp w: n 64*(w&1).. (4 groups of 8 (S,A) row pairs), fields 16*(w>>1)..
+// Consumer warp w: n 64*(w&1).. (4 groups of 8 (S,A) row pairs), fields 16*(w>>1)..
 struct DirTile {
   int lm, n0, f0, K, i0, nrings, nk, kp, nf;
   const double* P;
 };
 
+__device__ __forceinline__ DirTile dir_tile(const LegParams& p, int t) {
+  DirTile c;
+  const LegTile tile = p.tiles[t];
+  c.lm = tile.lm;
+  c.n0 = tile.r0;
+  c.f0 = tile.f0;
+  const int m = p.lm_m[c.lm];
+  c.i0 = p.lm_i0[c.lm];
+  c.kp = p.lm_kp[c.lm];
+  c.K = p.T - m + 1;
+  c.nrings = p.nh - c.i0;
+  c.nk = (c.nrings + kDirKcR - 1) / kDirKcR;
+  c.nf = min(kLegFields, p.nfld - c.f0);
+  c.P = p.ptab + p.lm_poff[c.lm];
+  return c;
+}
+
 __global__ void __launch_bounds__(kLegThreads, 1)
     leg_dir_kernel(const LegParams p, const double* __restrict__ four, double* __restrict__ spec) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ int s_tile;
-  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) Pipe pp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wn = warp & 1, wf = warp >> 1;
-  const int lr = lane >> 2, lc = lane & 3;
   const int64_t rowd = (int64_t)p.nfld * 4;
 
-  for (int i = tid; i < kStages * kDirStageDbl; i += kLegThreads) sm[i] = 0.0;
-  if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
-    fence_mbar_init();
-  }
+  for (int i = tid; i < kDirStages * kDirStageDbl; i += kLegThreads) sm[i] = 0.0;
+  pipe_init<kDirStages>(pp);
   fence_async_smem();
   __syncthreads();
 
-  auto make = [&](int t) {
-    DirTile c;
-    const LegTile tile = p.tiles[t];
-    c.lm = tile.lm;
-    c.n0 = tile.r0;
-    c.f0 = tile.f0;
-    const int m = p.lm_m[c.lm];
-    c.i0 = p.lm_i0[c.lm];
-    c.kp = p.lm_kp[c.lm];
-    c.K = p.T - m + 1;
-    c.nrings = p.nh - c.i0;
-    c.nk = (c.nrings + kDirKc - 1) / kDirKc;
-    c.nf = min(kLegFields, p.nfld - c.f0);
-    c.P = p.ptab + p.lm_poff[c.lm];
-    return c;
-  };
-  auto issue = [&](const DirTile& c, int kc, int st) {
-    if (p.debug & 1) return;
-    double* Ps = sm + st * kDirStageDbl;
-    double* Bs = Ps + kDirPDbl;
-    const int nr = min(kDirKc, c.nrings - kc * kDirKc);
-    const int pbytes = min(kDirN, c.kp - c.n0) * 8;
-    if (warp == 0) {
-      // rings past the end inside the last 4-ring k-step must contribute zero;
-      // the arrive (release) follows the zero stores
-      for (int rr = nr; rr < ((nr + 3) & ~3); ++rr)
-        for (int q = lane; q < kDirN; q += 32) Ps[rr * kDirPStr + q] = 0.0;
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(&full[st], (unsigned)(nr * (pbytes + c.nf * 32)));
+  if (warp == kConsumers) {  // ---- producer: per ring of the chunk one P-row segment and one Fourier row
+    int st = 0;
+    unsigned ph = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const DirTile c = dir_tile(p, t);
+      const int pbytes = min(kDirN, c.kp - c.n0) * 8;
+      for (int kc = 0; kc < c.nk; ++kc) {
+        mbar_wait(&pp.empty[st], ph ^ 1);
+        double* Ps = sm + st * kDirStageDbl;
+        double* Bs = Ps + kDirPDbl;
+        const int nr = min(kDirKcR, c.nrings - kc * kDirKcR);
+        // rings past the end inside the last 4-ring k-step must contribute
+        // zero; the expect_tx arrival (release) follows these stores
+        for (int rr = nr; rr < ((nr + 3) & ~3); ++rr)
+          for (int q = lane; q < kDirN; q += 32) Ps[rr * kDirPStr + q] = 0.0;
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&pp.full[st], (unsigned)(nr * (pbytes + c.nf * 32)));
+        __syncwarp();
+        for (int j = lane; j < 2 * nr; j += 32) {
+          const int rr = j >> 1;
+          const int ring = kc * kDirKcR + rr;  // relative to i0
+          if (j & 1)
+            bulk_g2s(Bs + rr * kDirBStr + dir_boff(rr), four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd +
+                     (int64_t)c.f0 * 4, c.nf * 32, &pp.full[st]);
+          else
+            bulk_g2s(Ps + rr * kDirPStr, c.P + (int64_t)ring * c.kp + c.n0, pbytes, &pp.full[st]);
+        }
+        if (++st == kDirStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
     }
-    for (int j = tid; j < 2 * nr; j += kLegThreads) {
-      const int rr = j >> 1;
-      const int ring = kc * kDirKc + rr;  // relative to i0
-      if (j & 1)
-        bulk_g2s(Bs + rr * kDirBStr, four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd + (int64_t)c.f0 * 4,
-                 c.nf * 32, &full[st]);
-      else
-        bulk_g2s(Ps + rr * kDirPStr, c.P + (int64_t)ring * c.kp + c.n0, pbytes, &full[st]);
-    }
-  };
-  auto prologue = [&](const DirTile& c) {
-    for (int st = 0; st < kStages && st < c.nk; ++st) issue(c, st, st);
-  };
+    return;
+  }
 
-  unsigned phase = 0;
-  if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-  __syncthreads();
-  int t = s_tile;
-  if (t >= p.ntiles) return;
-  DirTile c = make(t);
-  prologue(c);
-  while (true) {
+  const int wn = warp & 1, wf = warp >> 1;
+  const int lr = lane >> 2, lc = lane & 3;
+  int st = 0;
+  unsigned ph = 0;
+  for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    const DirTile c = dir_tile(p, t);
     double acc[4][2][4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g)
@@ -325,15 +356,13 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
 
     for (int kc = 0; kc < c.nk; ++kc) {
-      const int st = kc & 1;
-      if (!(p.debug & 1)) mbar_wait(&full[st], (phase >> st) & 1);
-      phase ^= 1u << st;
-      if (active && !(p.debug & 2)) {
+      mbar_wait(&pp.full[st], ph);
+      if (active) {
         const double* Ps = sm + st * kDirStageDbl + lc * kDirPStr + wn * 64 + 2 * lr;
-        const double* Bs = sm + st * kDirStageDbl + kDirPDbl + lc * kDirBStr + 4 * (wf * 16 + lr);
-        const int kmax = min(kDirKc / 4, (c.nrings - kc * kDirKc + 3) / 4);
+        const double* Bs = sm + st * kDirStageDbl + kDirPDbl + lc * kDirBStr + dir_boff(lc) + 4 * (wf * 16 + lr);
+        const int kmax = min(kDirKcR / 4, (c.nrings - kc * kDirKcR + 3) / 4);
 #pragma unroll
-        for (int ks = 0; ks < kDirKc / 4; ++ks) {
+        for (int ks = 0; ks < kDirKcR / 4; ++ks) {
           if (ks >= kmax) break;
           double2 a[4], bs[2], ba[2];
 #pragma unroll
@@ -358,16 +387,12 @@ __global__ void __launch_bounds__(kLegThreads, 1)
             }
         }
       }
-      __syncthreads();
-      if (kc + kStages < c.nk) issue(c, kc + kStages, st);
-    }
-    if (tid == 0) s_tile = atomicAdd(p.counter, 1);
-    __syncthreads();
-    const int tn = s_tile;
-    DirTile cn;
-    if (tn < p.ntiles) {
-      cn = make(tn);
-      prologue(cn);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pp.empty[st]);
+      if (++st == kDirStages) {
+        st = 0;
+        ph ^= 1;
+      }
     }
 
     if (active && !(p.debug & 4)) {
@@ -390,9 +415,6 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         }
       }
     }
-    if (tn >= p.ntiles) break;
-    c = cn;
-    __syncthreads();
   }
 }
 
@@ -476,8 +498,8 @@ __global__ void leg_poly_kernel(int T, int nh, int lm0, const int32_t* __restric
 
 }  // namespace
 
-size_t leg_inv_smem() { return (size_t)kStages * kInvStageDbl * sizeof(double); }
-size_t leg_dir_smem() { return (size_t)kStages * kDirStageDbl * sizeof(double); }
+size_t leg_inv_smem() { return (size_t)kInvStages * kInvStageDbl * sizeof(double); }
+size_t leg_dir_smem() { return (size_t)kDirStages * kDirStageDbl * sizeof(double); }
 
 void launch_leg_inv(const LegParams& p, const double* spec, double* four, int grid, cudaStream_t s) {
   // the attribute is per device: set it once for every device a plan runs on

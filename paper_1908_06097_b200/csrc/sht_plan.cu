@@ -38,7 +38,7 @@ int fail(int code, const std::string& msg) {
 #define SHT_NCCL_TRY(expr)                                                                           \
   do {                                                                                              \
     ncclResult_t _r = (expr);                                                                       \
-    if (_r != ncclSuccess) return ::sht::fail(SHT_ERR_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    if (_r != ncclSuccess && _r != ncclInProgress) return ::sht::fail(SHT_ERR_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
   } while (0)
 
 // ------------------------------------------------------------------ geometry
@@ -411,6 +411,37 @@ static int comm_check(sht_plan* p) {
   return SHT_OK;
 }
 
+// The plan's communicator is non-blocking (ncclConfig_t::blocking = 0), so no
+// NCCL call can hang the host on a dead peer: a call returns at once, maybe
+// with ncclInProgress, and nccl_settle polls its completion with the plan's
+// timeout, aborting the communicator when it expires.
+static int nccl_settle(sht_plan* p, ncclResult_t rc, const char* what) {
+  if (rc != ncclSuccess && rc != ncclInProgress)
+    return fail(SHT_ERR_COMM, std::string(what) + ": " + ncclGetErrorString(rc));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    ncclResult_t st = ncclSuccess;
+    if (ncclCommGetAsyncError(p->comm, &st) != ncclSuccess) st = ncclInternalError;
+    if (st == ncclSuccess) return SHT_OK;
+    if (st != ncclInProgress) {
+      p->failed = true;
+      p->fail_msg = std::string(what) + ": " + ncclGetErrorString(st);
+      return fail(SHT_ERR_COMM, p->fail_msg);
+    }
+    const uint64_t el = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            std::chrono::steady_clock::now() - t0).count();
+    if (el > p->timeout_ns) {
+      p->failed = true;
+      ncclCommAbort(p->comm);
+      p->comm = nullptr;
+      p->fail_msg = std::string(what) + " did not complete within " + std::to_string(p->timeout_ns / 1000000) +
+                    " ms; communicator aborted";
+      return fail(SHT_ERR_COMM, p->fail_msg);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 // Waits for stream `s` with a bound: polls the stream, the handshake error
 // word and NCCL's asynchronous error; on a peer failure or after
 // `timeout_ns` the plan is marked failed (its NCCL communicator is aborted at
@@ -456,8 +487,7 @@ static int close_barrier(sht_plan* p) {
   int* d = nullptr;
   int rc = SHT_OK;
   if (cudaMalloc((void**)&d, sizeof(int)) != cudaSuccess) rc = fail(SHT_ERR_CUDA, "cudaMalloc (close barrier)");
-  if (!rc && ncclAllReduce(d, d, 1, ncclInt, ncclSum, p->comm, s) != ncclSuccess)
-    rc = fail(SHT_ERR_COMM, "ncclAllReduce (close barrier)");
+  if (!rc) rc = nccl_settle(p, ncclAllReduce(d, d, 1, ncclInt, ncclSum, p->comm, s), "ncclAllReduce (close barrier)");
   if (!rc) rc = wait_stream(p, s, p->timeout_ns);
   if (d) cudaFree(d);
   cudaStreamDestroy(s);
@@ -499,8 +529,9 @@ static int build_transport(sht_plan* p) {
     std::vector<Rec> all(P);
     auto exchange = [&]() -> int {
       SHT_CUDA_TRY(cudaMemcpy(d + P, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
-      SHT_NCCL_TRY(ncclAllGather(d + P, d, sizeof(Rec), ncclChar, p->comm, 0));
-      SHT_CUDA_TRY(cudaStreamSynchronize(0));
+      if (int rc = nccl_settle(p, ncclAllGather(d + P, d, sizeof(Rec), ncclChar, p->comm, 0), "ncclAllGather (IPC handles)"))
+        return rc;
+      if (int rc = wait_stream(p, 0, p->timeout_ns)) return rc;
       SHT_CUDA_TRY(cudaMemcpy(all.data(), d, P * sizeof(Rec), cudaMemcpyDeviceToHost));
       return SHT_OK;
     };
@@ -871,7 +902,12 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     if (!nccl_id) return fail(SHT_ERR_CONFIG, "nranks > 1 needs an NCCL unique id");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
-    SHT_NCCL_TRY(ncclCommInitRank(&p->comm, P, id, r));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;  // never block the host on a dead peer (nccl_settle)
+    const ncclResult_t irc = ncclCommInitRankConfig(&p->comm, P, id, r, &cfg);
+    if (irc != ncclSuccess && irc != ncclInProgress)
+      return fail(SHT_ERR_COMM, std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(irc));
+    if (int rc = nccl_settle(p, ncclInProgress, "ncclCommInitRankConfig")) return rc;
   }
   return build_transport(p);
 }
@@ -929,6 +965,7 @@ static int alltoall(sht_plan* p, bool from_x, cudaStream_t s) {
   if (srows[r] > 0)
     SHT_CUDA_TRY(cudaMemcpyAsync(dst + doff[r] * rowd, src + soff[r] * rowd, srows[r] * rowd * sizeof(double),
                                  cudaMemcpyDeviceToDevice, s));
+  if (p->failed || !p->comm) return comm_check(p);
   SHT_NCCL_TRY(ncclGroupStart());
   for (int k = 1; k < P; ++k) {
     const int to = (r + k) % P, from = (r - k + P) % P;
@@ -937,8 +974,7 @@ static int alltoall(sht_plan* p, bool from_x, cudaStream_t s) {
     if (drows[from] > 0)
       SHT_NCCL_TRY(ncclRecv(dst + doff[from] * rowd, drows[from] * rowd, ncclDouble, from, p->comm, s));
   }
-  SHT_NCCL_TRY(ncclGroupEnd());
-  return SHT_OK;
+  return nccl_settle(p, ncclGroupEnd(), "ncclGroupEnd (transposition)");
 }
 
 static int check_ptr(const void* q, const char* what) {

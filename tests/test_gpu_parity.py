@@ -203,3 +203,86 @@ def test_recompute_legendre_matches_table(torch, monkeypatch):
 
 def test_parity_tco1279(torch):
     _check(torch, 1279, 2)
+
+
+BENCH_FIELDS = [0, 1, 63, 64, 127, 128, 511, 547]
+
+
+def test_oneway_bench_config_sampled_fields(torch):
+    """The bench workload itself (TCo639 x 548 fields): one-way inv_trans and dir_trans vs the
+    oracle on fields across the 64-field Legendre tiles and FFT batches ({0, 1, 63, 64, 127, 128,
+    511, 547}: first/last of tiles, the ragged last tile).  The oracle is per-field independent,
+    so it runs on those 8 fields only."""
+    from oracle.sht_oracle import SHTransformOracle, random_grid, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 639, 548
+    sh = SHTransform(T, nfld=nf)
+    a = random_spectral(T, nf, seed=11)
+    o = SHTransformOracle(T, nfld=len(BENCH_FIELDS))
+    g = random_grid(T, nf, o.npts, seed=12)
+    gi = sh.inv_trans(torch.from_numpy(a).cuda())[BENCH_FIELDS].cpu().numpy()
+    sd = sh.dir_trans(torch.from_numpy(g).cuda())[BENCH_FIELDS].cpu().numpy()
+    e_inv = rel(gi, o.inv_trans(a[BENCH_FIELDS]))
+    e_dir = rel(sd, o.dir_trans(g[BENCH_FIELDS]))
+    assert e_inv <= TOL and e_dir <= TOL, (e_inv, e_dir)
+
+
+TCO1999_M = [0, 1, 2, 3, 500, 999, 1000, 1001, 1500, 1997, 1998, 1999]
+
+
+@pytest.mark.parametrize("recompute", [False, True])
+def test_parity_tco1999_m_subset(torch, recompute):
+    """TCo1999 (the memory-capacity config, 26.75 GB stored table or chunked recompute): one-way
+    transforms vs the oracle restricted to a set of wavenumbers across the range (the full oracle
+    table would need 27 GB of host RAM).  inv: spectral input nonzero only on those m; dir: the
+    coefficients of those m from a full random grid."""
+    from oracle.sht_oracle import SHTransformOracle, random_grid, random_spectral, spec_offsets
+    from paper_1908_06097_b200 import SHTransform
+
+    T, nf = 1999, 2
+    o = SHTransformOracle(T, nfld=nf, m_subset=TCO1999_M)
+    sh = SHTransform(T, nfld=nf, recompute_legendre=recompute)
+    soff = spec_offsets(T)
+    keep = np.zeros(sh.nspec_local, dtype=bool)
+    for m in TCO1999_M:
+        keep[2 * soff[m]: 2 * soff[m + 1]] = True
+    a = random_spectral(T, nf, seed=5)
+    a[:, ~keep] = 0.0
+    g = random_grid(T, nf, o.npts, seed=6)
+    e_inv = rel(sh.inv_trans(torch.from_numpy(a).cuda()).cpu().numpy(), o.inv_trans(a))
+    sd = sh.dir_trans(torch.from_numpy(g).cuda()).cpu().numpy()
+    e_dir = rel(sd[:, keep], o.dir_trans(g)[:, keep])
+    assert e_inv <= TOL and e_dir <= TOL, (e_inv, e_dir)
+
+
+def test_gpu_vs_brute_force_synthesis(torch):
+    """GPU transforms vs pointwise synthesis / explicit quadrature with scipy's Pbar (no FFT, no
+    recurrence shared with the kernels): independent of the oracle."""
+    from oracle.sht_oracle import gauss_nodes, octahedral_nloen, random_grid, random_spectral
+    from paper_1908_06097_b200 import SHTransform
+    from oracle.brute import brute_analysis, brute_synthesis
+
+    T, nf = 31, 3
+    nloen = octahedral_nloen(T)
+    mu, _, w = gauss_nodes(2 * T + 2)
+    mu_all = np.concatenate([mu, -mu[::-1]])
+    w_all = np.concatenate([w, w[::-1]])
+    sh = SHTransform(T, nfld=nf)
+    a = random_spectral(T, nf, seed=21)
+    g = random_grid(T, nf, int(nloen.sum()), seed=22)
+    e_inv = rel(sh.inv_trans(torch.from_numpy(a).cuda()).cpu().numpy(), brute_synthesis(T, a, nloen, mu_all))
+    e_dir = rel(sh.dir_trans(torch.from_numpy(g).cuda()).cpu().numpy(), brute_analysis(T, g, nloen, mu_all, w_all))
+    assert e_inv <= TOL and e_dir <= TOL, (e_inv, e_dir)
+
+
+def test_parity_factor_local_bluestein(torch):
+    """Rings whose whole-ring Bluestein length would exceed one CTA (odd n = 7 x 1031 = 7217:
+    2n - 1 > 12288, no pruning for odd n) take the factor-local Bluestein step for the prime
+    1031 (bluestein_step in sht_fft.cu), which no octahedral config reaches."""
+    from paper_1908_06097_b200 import fft_plan_info
+
+    info = fft_plan_info(7217)
+    assert info["bluestein"] and info["length"] == 7217 and 1031 in info["radices"]
+    T = 15
+    _check(torch, T, 2, grid=np.full(2 * (T + 1), 7217))

@@ -159,3 +159,41 @@ def test_custom_grid_regular_gaussian():
 def test_bad_grid():
     with pytest.raises(ValueError):
         SHTransformOracle(10, grid=np.array([20, 24, 20]), nfld=1)
+
+
+# ---------------------------------------------------------------- brute-force pins (no FFT, no recurrence)
+from oracle.brute import brute_analysis, brute_synthesis  # noqa: E402
+
+
+@pytest.mark.parametrize("T", [23, 31])
+def test_oracle_vs_brute_force(T):
+    """The oracle's inverse and direct transforms equal pointwise synthesis / quadrature by explicit
+    sums over all (n, m) with scipy's Pbar -- no FFT and no shared recurrence (pins the conventions
+    beyond the l <= 1 KATs)."""
+    o = SHTransformOracle(T, nfld=3)
+    mu, _, w = gauss_nodes(2 * T + 2)
+    mu_all = np.concatenate([mu, -mu[::-1]])
+    w_all = np.concatenate([w, w[::-1]])
+    a = random_spectral(T, 3, seed=7)
+    g = random_grid(T, 3, o.npts, seed=8)
+    fb = brute_synthesis(T, a, o.nloen, mu_all)
+    assert np.max(np.abs(o.inv_trans(a) - fb)) <= 1e-12 * np.max(np.abs(fb))
+    sb = brute_analysis(T, g, o.nloen, mu_all, w_all)
+    assert np.max(np.abs(o.dir_trans(g) - sb)) <= 1e-12 * np.max(np.abs(sb))
+
+
+def test_oracle_m_subset_matches_full():
+    """m_subset restricts the oracle to a few wavenumbers (the TCo1999 parity tests use it)."""
+    T, S = 47, [0, 1, 5, 30, 47]
+    full = SHTransformOracle(T, nfld=2)
+    sub = SHTransformOracle(T, nfld=2, m_subset=S)
+    a = random_spectral(T, 2, seed=3)
+    soff = np.arange(T + 2) * (2 * T - np.arange(T + 2) + 3) // 2
+    keep = np.zeros(a.shape[1], dtype=bool)
+    for m in S:
+        keep[2 * soff[m]: 2 * soff[m + 1]] = True
+    a[:, ~keep] = 0.0
+    assert np.max(np.abs(sub.inv_trans(a) - full.inv_trans(a))) <= 1e-15 * np.max(np.abs(full.inv_trans(a)))
+    g = random_grid(T, 2, full.npts, seed=4)
+    ds, df = sub.dir_trans(g), full.dir_trans(g)
+    assert np.array_equal(ds[:, keep], df[:, keep]) and not ds[:, ~keep].any()

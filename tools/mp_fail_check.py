@@ -34,10 +34,17 @@ def main():
         print(f"rank {rank}: dying now", flush=True)
         os._exit(0)
     t0 = time.time()
+    dbg = os.environ.get("MP_FAIL_DEBUG") == "1"
     try:
-        for _ in range(3):
+        for i in range(3):
+            if dbg:
+                print(f"rank {rank}: pair {i} inv", flush=True)
             sh.inv_trans(spec, out=grid)
+            if dbg:
+                print(f"rank {rank}: pair {i} dir", flush=True)
             sh.dir_trans(grid, out=spec)
+        if dbg:
+            print(f"rank {rank}: synchronize", flush=True)
         sh.synchronize()
         print(f"rank {rank}: no error after {time.time() - t0:.1f}s", flush=True)
         ok = False
