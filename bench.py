@@ -46,12 +46,61 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--truncation", type=int, default=639)
     ap.add_argument("--nfld", type=int, default=548)
-    ap.add_argument("--cpu-fields", type=int, default=16, help="fields in the bounded CPU sample")
+    ap.add_argument("--cpu-fields", type=int, default=137,
+                    help="fields in the bounded CPU sample (137 = one model level set of the 548-field batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--recompute-legendre", action="store_true",
                     help="regenerate the P table chunk by chunk every transform (TCo1999 memory mode)")
     return ap.parse_args()
+
+
+DEBUG_VARS = ("SHT_FFT_DEBUG", "SHT_LEG_DEBUG")
+
+
+def refuse_debug() -> None:
+    """Profiling switches that skip work inside the product kernels void a bench number."""
+    bad = [v for v in DEBUG_VARS if os.environ.get(v, "0") not in ("", "0")]
+    if bad:
+        raise SystemExit(f"bench.py refuses to run with {', '.join(bad)} set (they skip work inside the kernels)")
+
+
+def lscpu() -> dict:
+    out = {"os_cpu_count": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)",
+                             "NUMA node(s)", "CPU max MHz"):
+                out[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return out
+
+
+def window_average(samples, t0: float, t1: float) -> float:
+    """Mean power over [t0, t1], each sample held until the next one and the first one extended
+    backwards -- a restatement of the reference's haloflow.energy.window_average
+    (/root/reference/pkg/src/haloflow/energy.py:83-111); tests/test_bench.py checks it against the
+    reference's own function."""
+    if t1 <= t0 or not samples:
+        raise ValueError("empty window or no samples")
+    times = [t for t, _ in samples]
+    if any(b <= a for a, b in zip(times, times[1:])):
+        raise ValueError("samples must be in strictly increasing time order")
+    import bisect
+
+    joules, cursor = 0.0, t0
+    while cursor < t1:
+        i = max(bisect.bisect_right(times, cursor) - 1, 0)
+        seg_end = times[i + 1] if i + 1 < len(times) else t1
+        seg_end = min(max(seg_end, cursor), t1)
+        if seg_end == cursor:
+            seg_end = t1
+        joules += samples[i][1] * (seg_end - cursor)
+        cursor = seg_end
+    return joules / (t1 - t0)
 
 
 def peaks() -> dict:
@@ -77,9 +126,9 @@ def peaks() -> dict:
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (rank 0)."""
+    """nvidia-smi sampler of one GPU running during the timed region (every rank samples its own)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -92,7 +141,7 @@ class Clocks:
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
-        self.skip = 0
+        self.t0 = self.t1 = None
         # NVML start-up must be over before the timed region: wait for the first samples
         t0 = time.perf_counter()
         while self.p is not None and time.perf_counter() - t0 < 5.0:
@@ -101,36 +150,49 @@ class Clocks:
             time.sleep(0.01)
 
     def mark(self) -> None:
-        """Start of the timed region: later samples are the ones that count."""
-        self.skip = Path(self.f.name).stat().st_size
+        """Start of the timed region (host wall clock, the clock nvidia-smi stamps with)."""
+        self.t0 = time.time()
+
+    def end(self) -> None:
+        self.t1 = time.time()
 
     def stop(self) -> dict | None:
         if self.p is None:
             return None
+        time.sleep(0.25)  # one more sample after the window
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         txt = Path(self.f.name).read_text()
-        rows = [r.split(",") for r in txt[self.skip:].splitlines() if r.strip()]
-        if not rows:  # a timed region shorter than the sampling period: the sample that bracketed it
-            rows = [r.split(",") for r in txt.splitlines() if r.strip()][-1:]
         os.unlink(self.f.name)
-        sm, mx, reasons, pw = [], 0.0, set(), []
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in rows:
+        from datetime import datetime
+
+        rows = []
+        for r in txt.splitlines():
+            c = [x.strip() for x in r.split(",")]
             try:
-                sm.append(float(r[1]))
-                mx = max(mx, float(r[2]))
-                pw.append(float(r[3]))
-                for k, nm in enumerate(names):
-                    if r[4 + k].strip().lower() == "active":
-                        reasons.add(nm)
+                t = datetime.strptime(c[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((t, float(c[2]), float(c[3]), float(c[4]), c[5:9]))
             except (ValueError, IndexError):
                 continue
-        if not sm:
+        if not rows:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
-                "power_w": float(np.mean(pw)) if pw else None}
+        t0, t1 = self.t0 or rows[0][0], self.t1 or rows[-1][0]
+        inside = [r for r in rows if t0 <= r[0] <= t1] or [min(rows, key=lambda r: abs(r[0] - t1))]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({nm for r in inside for nm, v in zip(names, r[4]) if v.lower() == "active"})
+        power = [(r[0], r[3]) for r in rows]
+        dedup = []
+        for t, w in power:  # strictly increasing timestamps for window_average
+            if not dedup or t > dedup[-1][0]:
+                dedup.append((t, w))
+        try:
+            avg_w = window_average(dedup, t0, t1) if t1 > t0 else dedup[-1][1]
+        except ValueError:
+            avg_w = None
+        return {"gpu": self.idx, "sm_mhz": float(np.median([r[1] for r in inside])),
+                "sm_max_mhz": max(r[2] for r in inside), "reasons": reasons, "samples": len(inside),
+                "power_w_window_avg": avg_w, "window_s": t1 - t0}
 
 
 def dist_setup():
@@ -188,14 +250,23 @@ def cpu_oracle_pair_ms(T: int, nfld_sample: int, nfld_full: int, pairs: int = 1,
     return per * nfld_full / nfld_sample, per, times
 
 
-def traffic_per_launch(kernel: str):
+def traffic_per_launch(kernel: str, T: int, nfld: int, P: int, mode: str):
+    """DRAM bytes (read + write) per launch of `kernel` from an `ncu --set full` capture of this exact
+    configuration (profiles/traffic.json, keyed "TCo{T}_nfld{nfld}_P{P}_{mode}"), else None."""
     f = ROOT / "profiles" / "traffic.json"
     if f.exists():
         try:
-            return json.loads(f.read_text()).get(kernel)
+            return json.loads(f.read_text()).get(f"TCo{T}_nfld{nfld}_P{P}_{mode}", {}).get(kernel)
         except Exception:
             return None
     return None
+
+
+def config_of(args) -> dict:
+    """The workload keys both arms report (identical, so the driver can match them)."""
+    T, nf = args.truncation, args.nfld
+    return {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
+            "grid": "octahedral"}
 
 
 def run_reference(args):
@@ -208,7 +279,8 @@ def run_reference(args):
 
     o = SHTransformOracle(T, nfld=ns, workers=cores)
     a = random_spectral(T, ns)
-    for _ in range(args.warmup):
+    warm = min(args.warmup, 1)  # one warm-up pair: the CPU path has no caches worth more
+    for _ in range(warm):
         o.dir_trans(o.inv_trans(a))
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -216,14 +288,15 @@ def run_reference(args):
     per_sample = (time.perf_counter() - t0) * 1e3 / args.steps
     value = per_sample * nf / ns
     sample = (f"TCo{T}, {ns} of {nf} fields per inv+dir pair (CPU oracle oracle/sht_oracle.py: NumPy BLAS "
-              f"Legendre GEMMs + scipy.fft ring FFTs, workers={cores}), time scaled x{nf}/{ns} (linear in fields)")
+              f"Legendre GEMMs + scipy.fft ring FFTs, workers={cores}), time scaled x{nf}/{ns} (linear in fields); "
+              f"{warm} warm-up pair(s)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
-                   "grid": "octahedral"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": config_of(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "lscpu": lscpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (haloflow) has no transform code (SPEC.md:20); its CPU path is the oracle port",
     }
@@ -237,6 +310,7 @@ def run_ours(args):
 
     from paper_1908_06097_b200 import SHTransform
 
+    refuse_debug()
     rank, world, local = dist_setup()
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -260,23 +334,28 @@ def run_ours(args):
         sh.inv_trans(spec, out=grid)
         sh.dir_trans(grid, out=spec2)
 
-    clk = Clocks(local) if rank == 0 else None  # started before the warm-up (NVML start-up)
+    clk = Clocks(local)  # every rank samples its own GPU; started before the warm-up (NVML start-up)
     for _ in range(args.warmup):
         pair()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if clk:
-        clk.mark()
+    clk.mark()
     e0.record()
     for _ in range(args.steps):
         pair()
     e1.record()
     torch.cuda.synchronize()
+    clk.end()
     if world > 1:
         dist.barrier()
-    clocks = clk.stop() if clk else None
+    clk_local = clk.stop()
+    if world > 1:
+        allc = [None] * world
+        dist.all_gather_object(allc, clk_local)
+    else:
+        allc = [clk_local]
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world)
     ph = sh.phase_ms(min(args.steps, 64))
@@ -317,31 +396,44 @@ def run_ours(args):
     t_fft_roof = B_fft / (pk["hbm_gbs"] * 1e9) * 1e3
     transport = sh.transport
     t_a2a_roof = B_a2a / (pk["nvlink_gbs"] * 1e9) * 1e3 if world > 1 else 0.0
-    # p2p: the NVLink stores run inside the Legendre / FFT kernels, so the
-    # transfer adds no time of its own to the bound; nccl: it is serialised
-    t_roof = t_leg_roof + t_fft_roof + (t_a2a_roof if transport == "nccl" else 0.0)
+    p2p = transport == "p2p"
+    # p2p: the NVLink stores run inside the producing kernels (leg_inv -> ring owners, fft_g2f -> m
+    # owners), so each of those is bounded by max(its own work / its peak, its NVLink bytes / 770 GB/s)
+    # (B200_PROFILING.md fused compute+collective roofline); nccl: the transfer is a phase of its own
+    t_a2a_dir = t_a2a_roof / 2
+    t_roof = (max(t_leg_roof / 2, t_a2a_dir if p2p else 0.0) + t_leg_roof / 2 +
+              t_fft_roof / 2 + max(t_fft_roof / 2, t_a2a_dir if p2p else 0.0) + (0.0 if p2p else t_a2a_roof))
 
-    # per-kernel rooflines (each direction's kernel = one logical launch; the
-    # ring FFT is split over launch classes by shared-memory footprint)
     def mx(v):
         return max_over_ranks(v, world)
 
+    mode = "recompute" if args.recompute_legendre else "table"
+    nvl = B_a2a / 2 if p2p else 0.0  # bytes one rank stores into its peers per direction
     kern = {
-        "leg_inv_kernel": ("tensor", mx(ph["inv_legendre"]), F_leg / 2 / 1e12, "TFLOP/s", pk["fp64_tflops"],
-                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop (4*NFLD*sum_m NDGLU(m)(T-m+1) per direction)"),
-        "leg_dir_kernel": ("tensor", mx(ph["dir_legendre"]), F_leg / 2 / 1e12, "TFLOP/s", pk["fp64_tflops"],
-                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop"),
-        "fft_f2g": ("hbm", mx(ph["inv_fft"]), B_fft / 2 / 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
-                    f"{B_fft / 2:.4e} B (grid 8 B x 2 N_i + Fourier rows 32 B x (M_i+1), per field and ring pair)"),
-        "fft_g2f": ("hbm", mx(ph["dir_fft"]), B_fft / 2 / 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
-                    f"{B_fft / 2:.4e} B"),
+        "leg_inv_kernel": ("tensor", mx(ph["inv_legendre"]), F_leg / 2, 1e12, "TFLOP/s", pk["fp64_tflops"],
+                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop (4*NFLD*sum_m NDGLU(m)(T-m+1) per direction)",
+                           nvl),
+        "leg_dir_kernel": ("tensor", mx(ph["dir_legendre"]), F_leg / 2, 1e12, "TFLOP/s", pk["fp64_tflops"],
+                           pk["fp64_src"], f"{F_leg / 2:.4e} FP64 flop", 0.0),
+        "fft_f2g": ("hbm", mx(ph["inv_fft"]), B_fft / 2, 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
+                    f"{B_fft / 2:.4e} B (grid 8 B x 2 N_i + Fourier rows 32 B x (M_i+1), per field and ring pair)",
+                    0.0),
+        "fft_g2f": ("hbm", mx(ph["dir_fft"]), B_fft / 2, 1e9, "GB/s", pk["hbm_gbs"], pk["hbm_src"],
+                    f"{B_fft / 2:.4e} B", nvl),
     }
     rooflines = {}
-    for name, (bound, t_ms, amount, unit, peak, src, per) in kern.items():
-        ach = amount / (t_ms * 1e-3) if t_ms > 0 else 0.0
-        rooflines[name] = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit,
-                           "frac": ach / peak, "traffic": traffic_per_launch(name), "ms": t_ms, "peak_src": src,
-                           "per_launch": per}
+    for name, (bound, t_ms, amount, scale, unit, peak, src, per, nvbytes) in kern.items():
+        ach = amount / scale / (t_ms * 1e-3) if t_ms > 0 else 0.0
+        r = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+             "traffic": traffic_per_launch(name, T, nf, world, mode), "ms": t_ms, "peak_src": src,
+             "per_launch": per}
+        if nvbytes > 0:  # fused compute + NVLink stores: the slower of the two ceilings
+            t_work = amount / scale / peak * 1e3
+            t_nvl = nvbytes / (pk["nvlink_gbs"] * 1e9) * 1e3
+            r["fused_nvlink"] = {"nvlink_bytes": nvbytes, "t_work_ms": t_work, "t_nvlink_ms": t_nvl,
+                                 "t_roof_ms": max(t_work, t_nvl), "frac": max(t_work, t_nvl) / t_ms if t_ms else None,
+                                 "nvlink_gbs_achieved": nvbytes / (t_ms * 1e-3) / 1e9 if t_ms else None}
+        rooflines[name] = r
     dom = max(rooflines, key=lambda k: rooflines[k]["ms"])
 
     cpu = None
@@ -349,17 +441,20 @@ def run_ours(args):
         full, per, _ = cpu_oracle_pair_ms(T, args.cpu_fields, nf, pairs=1, warm=0)
         cpu = {"value": full, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                "sample": f"TCo{T}, {args.cpu_fields} of {nf} fields, one inv+dir pair of the CPU oracle "
-                         f"(NumPy BLAS + scipy.fft, all host threads) = {per:.1f} ms, scaled x{nf}/{args.cpu_fields}"}
+                         f"(NumPy BLAS + scipy.fft, all host threads) = {per:.1f} ms, scaled x{nf}/{args.cpu_fields}",
+               "lscpu": lscpu()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"TCo{T} inverse+direct pair, {nf} fields", "truncation": T, "nfld": nf,
-                       "grid": "octahedral", "parallelism": f"m/ring-pair sharded x{world}, transposition: {transport}",
+            "config": config_of(args),
+            "layout": {"parallelism": f"m/ring-pair sharded x{world}, transposition: {transport}",
+                       "transport_env": os.environ.get("SHT_TRANSPORT", "p2p (default)"),
                        "legendre": "recomputed per transform" if args.recompute_legendre else "stored table",
-                       "l2": "inputs larger than L2 (spectral 1.8 GB, grid 7.3 GB per pair at 1 GPU)"},
+                       "l2": (f"no flush: inputs larger than L2 (spectral {spec.numel() * 8 / 1e9:.2f} GB, grid "
+                              f"{grid.numel() * 8 / 1e9:.2f} GB per rank vs 126 MB L2)")},
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "roofline": rooflines[dom],
@@ -376,14 +471,20 @@ def run_ours(args):
             "phases_ms": ph,
             "setup_s": setup_s,
             "cpu_baseline": cpu,
-            "clocks": clocks,
-            # SURVEY.md 8f row 3 (energy.py:83-119 energy_per_step): NVML board power of rank 0's GPU
-            # during the timed region x ms per pair, times the GPU count for the job
-            "energy": ({"j_per_pair": clocks["power_w"] * ms * 1e-3 * world, "avg_power_w_per_gpu": clocks["power_w"],
-                        "basis": "rank-0 GPU NVML power.draw mean over the timed region x n_gpus"}
-                       if clocks and clocks.get("power_w") else None),
+            "clocks": ({"sm_mhz": float(np.median([c["sm_mhz"] for c in allc if c])),
+                        "sm_max_mhz": max(c["sm_max_mhz"] for c in allc if c),
+                        "reasons": sorted({r for c in allc if c for r in c["reasons"]}),
+                        "per_gpu": allc} if any(allc) else None),
+            # per-GPU NVML power, each averaged over the timed window with the
+            # reference's window_average (energy.py:83-111), summed over GPUs x ms per pair
+            # (energy_per_step, energy.py:114-123)
+            "energy": ({"j_per_pair": sum(c["power_w_window_avg"] for c in allc) * ms * 1e-3,
+                        "power_w_per_gpu": [c["power_w_window_avg"] for c in allc],
+                        "basis": "per-GPU nvidia-smi power.draw, window_average over the timed region"}
+                       if all(c and c.get("power_w_window_avg") for c in allc) else None),
         }
         print(json.dumps(line), flush=True)
+    sh.close()  # collective: every rank releases its plan after the peers are done with it
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

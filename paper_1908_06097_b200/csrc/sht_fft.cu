@@ -569,6 +569,17 @@ static void launch_one(bool g2f, const FftParams& p, int w0, int nw, const doubl
   }
 }
 
+// Loads every FFT kernel now (cudaFuncGetAttributes forces the lazy module
+// load): a first launch inside a transform could otherwise block behind a
+// kernel spinning on a dead peer.
+void fft_preload() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, fft_g2f_kernel<1>);
+  cudaFuncGetAttributes(&a, fft_g2f_kernel<2>);
+  cudaFuncGetAttributes(&a, fft_f2g_kernel<1>);
+  cudaFuncGetAttributes(&a, fft_f2g_kernel<2>);
+}
+
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s) {
   if (nw <= 0) return;

@@ -81,6 +81,7 @@ void launch_leg_poly(int T, int nh, int lm0, int lm1, const int32_t* lm_m, const
                      const int64_t* lm_poff, const int32_t* lm_kp, const double* mu, const double* dmant,
                      const int32_t* dexp, double* ptab, cudaStream_t s);
 size_t leg_inv_smem();
+void leg_preload();  // load every kernel of the file now (no lazy load inside a transform)
 size_t leg_dir_smem();
 
 // ---------------------------------------------------------------- ring FFTs
@@ -153,6 +154,7 @@ struct FftParams {
 // (2 CTAs/SM); 2 = pencils up to 31 points (primes 17..31), 1 CTA/SM;
 // 3 = class-1 kernel with up to 212 KB of shared memory (1 CTA/SM).
 constexpr int kFftVariants = 4;  // index 0 unused
+void fft_preload();  // load every kernel of the file now (no lazy load inside a transform)
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s);
 

@@ -189,6 +189,13 @@ __global__ void __launch_bounds__(kLegThreads, 1)
     // warp-uniform trims of the ragged edges: 8-ring groups, 8-field groups, 8-n sub-steps
     const int gmax = min(4, max(0, (p.nh - c.r0 - wr * 32 + 7) / 8));
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
+    // the epilogue's destination rows, fetched now so their latency hides under the K loop
+    double* dst_row[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int ring = c.r0 + wr * 32 + g * 8 + (lane >> 2);
+      dst_row[g] = (active && ring < p.nh) ? p.ring_out[ring] : nullptr;
+    }
 
     for (int kc = 0; kc < c.nk; ++kc) {
       mbar_wait(&pp.full[st], ph);
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kLegThreads, 1)
       for (int g = 0; g < 4; ++g) {
         const int ring = c.r0 + wr * 32 + g * 8 + lr;
         if (ring < p.nh) {
-          double* dst = p.ring_out[ring] + (int64_t)c.lm * rowd;
+          double* dst = dst_row[g] + (int64_t)c.lm * rowd;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -523,6 +530,14 @@ void launch_leg_dir(const LegParams& p, const double* four, double* spec, int gr
     if (dev < 64) done |= 1ull << dev;
   }
   leg_dir_kernel<<<grid, kLegThreads, leg_dir_smem(), s>>>(p, four, spec);
+}
+
+void leg_preload() {  // see fft_preload
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, leg_inv_kernel);
+  cudaFuncGetAttributes(&a, leg_dir_kernel);
+  cudaFuncGetAttributes(&a, leg_poly_kernel);
+  cudaFuncGetAttributes(&a, leg_diag_kernel);
 }
 
 void launch_leg_diag(int T, int nh, int nlm, const int32_t* lm_m, const double* sint, double* dmant, int32_t* dexp,

@@ -19,6 +19,7 @@
 #include <thread>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -39,6 +40,19 @@ int fail(int code, const std::string& msg) {
   do {                                                                                              \
     ncclResult_t _r = (expr);                                                                       \
     if (_r != ncclSuccess && _r != ncclInProgress) return ::sht::fail(SHT_ERR_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+// Communication trace on stderr (SHT_DEBUG_COMM=1): failure-path diagnostics only.
+static bool comm_debug() {
+  static const bool d = getenv("SHT_DEBUG_COMM") != nullptr;
+  return d;
+}
+#define SHT_COMM_LOG(...)                         \
+  do {                                            \
+    if (comm_debug()) {                           \
+      fprintf(stderr, "[sht comm] " __VA_ARGS__); \
+      fflush(stderr);                             \
+    }                                             \
   } while (0)
 
 // ------------------------------------------------------------------ geometry
@@ -384,6 +398,11 @@ __global__ void flag_kernel(uint32_t* const* peer_flags, const uint32_t* flags, 
   }
 }
 
+void flag_preload() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, flag_kernel);
+}
+
 static int flags_op(sht_plan* p, int sig_slot, uint32_t sig_v, int wait_slot, uint32_t wait_v, cudaStream_t s) {
   flag_kernel<<<1, 32 * ((p->nranks + 31) / 32), 0, s>>>(p->d_peer_flags, p->flagw, p->nranks, p->rank, sig_slot,
                                                           sig_v, wait_slot, wait_v, p->timeout_ns, p->d_err);
@@ -394,6 +413,7 @@ static int flags_op(sht_plan* p, int sig_slot, uint32_t sig_v, int wait_slot, ui
 // Host-side view of the plan's communication health: the handshake error
 // word (written by flag_kernel) and NCCL's asynchronous error state.
 static int comm_check(sht_plan* p) {
+  SHT_COMM_LOG("rank %d: comm_check\n", p->rank);
   if (p->failed) return fail(SHT_ERR_COMM, "the plan failed earlier (" + p->fail_msg + "); close it");
   if (p->h_err && p->h_err[0] != 0) {
     const int v = p->h_err[0];
@@ -403,11 +423,8 @@ static int comm_check(sht_plan* p) {
                                   " ms waiting for rank " + std::to_string(v / 16 - 1) + " (" + slot[(v % 16) & 3] +
                                   "); the peer is dead or desynchronised");
   }
-  if (p->comm) {
-    ncclResult_t st = ncclSuccess;
-    if (ncclCommGetAsyncError(p->comm, &st) == ncclSuccess && st != ncclSuccess && st != ncclInProgress)
-      return fail(SHT_ERR_COMM, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st));
-  }
+  // (ncclCommGetAsyncError is polled only right after an NCCL call, in
+  // nccl_settle: with a dead peer it can block inside NCCL's progress engine)
   return SHT_OK;
 }
 
@@ -416,6 +433,7 @@ static int comm_check(sht_plan* p) {
 // with ncclInProgress, and nccl_settle polls its completion with the plan's
 // timeout, aborting the communicator when it expires.
 static int nccl_settle(sht_plan* p, ncclResult_t rc, const char* what) {
+  SHT_COMM_LOG("rank %d: %s returned %d\n", p->rank, what, (int)rc);
   if (rc != ncclSuccess && rc != ncclInProgress)
     return fail(SHT_ERR_COMM, std::string(what) + ": " + ncclGetErrorString(rc));
   const auto t0 = std::chrono::steady_clock::now();
@@ -432,7 +450,9 @@ static int nccl_settle(sht_plan* p, ncclResult_t rc, const char* what) {
                             std::chrono::steady_clock::now() - t0).count();
     if (el > p->timeout_ns) {
       p->failed = true;
+      SHT_COMM_LOG("rank %d: %s timed out, aborting the communicator\n", p->rank, what);
       ncclCommAbort(p->comm);
+      SHT_COMM_LOG("rank %d: communicator aborted\n", p->rank);
       p->comm = nullptr;
       p->fail_msg = std::string(what) + " did not complete within " + std::to_string(p->timeout_ns / 1000000) +
                     " ms; communicator aborted";
@@ -455,6 +475,7 @@ static int wait_stream(sht_plan* p, cudaStream_t s, uint64_t timeout_ns) {
     if (int rc = comm_check(p)) {
       p->failed = true;
       p->fail_msg = g_err;
+      SHT_COMM_LOG("rank %d: handshake failure seen by the wait, aborting\n", p->rank);
       if (p->comm) ncclCommAbort(p->comm), p->comm = nullptr;
       return rc;
     }
@@ -462,7 +483,9 @@ static int wait_stream(sht_plan* p, cudaStream_t s, uint64_t timeout_ns) {
                             std::chrono::steady_clock::now() - t0).count();
     if (el > timeout_ns) {
       p->failed = true;
+      SHT_COMM_LOG("rank %d: wait timed out, aborting\n", p->rank);
       if (p->comm) ncclCommAbort(p->comm), p->comm = nullptr;
+      SHT_COMM_LOG("rank %d: aborted\n", p->rank);
       p->fail_msg = "transform did not complete within " + std::to_string(timeout_ns / 1000000) +
                     " ms (a peer is dead or desynchronised); communicator aborted";
       return fail(SHT_ERR_COMM, p->fail_msg);
@@ -818,6 +841,9 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   if (dry_run) return SHT_OK;
 
   // ---- device side
+  fft_preload();
+  leg_preload();
+  flag_preload();
   int dev = 0;
   SHT_CUDA_TRY(cudaGetDevice(&dev));
   SHT_CUDA_TRY(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -966,6 +992,7 @@ static int alltoall(sht_plan* p, bool from_x, cudaStream_t s) {
     SHT_CUDA_TRY(cudaMemcpyAsync(dst + doff[r] * rowd, src + soff[r] * rowd, srows[r] * rowd * sizeof(double),
                                  cudaMemcpyDeviceToDevice, s));
   if (p->failed || !p->comm) return comm_check(p);
+  SHT_COMM_LOG("rank %d: all-to-all %s: group start\n", p->rank, from_x ? "X->Y" : "Y->X");
   SHT_NCCL_TRY(ncclGroupStart());
   for (int k = 1; k < P; ++k) {
     const int to = (r + k) % P, from = (r - k + P) % P;
