@@ -92,21 +92,32 @@ def _bluestein_len(lo: int, lmax: int = 1 << 30):
 
 
 def ring_fft_cost(n: int, mcap: int) -> int:
-    """Cost of one ring pair's FFTs per field: 3 per element-step + grid and row bytes."""
+    """Cost of one ring pair's FFTs per field: 3 per element-step + grid and row bytes.
+
+    Plans (libsht's fft_plan_ring): pencils <= 16 plus at most one prime 17..127 as a DMMA
+    prime step (~p/16 element-steps per point), <= 4 steps; else whole-ring Bluestein (pruned for
+    even n) when it fits one CTA, else factor-local Bluestein steps (~6 extra element-steps)."""
     primes, _ = _factor(n, n)
-    big = [p for p in primes if p > 31]
-    if big:  # whole-ring Bluestein; even n keeping |k| <= mcap needs only n + 2 mcap lags
-        pruned = n % 2 == 0 and n + 2 * mcap < 2 * n - 1
-        lo = n + 2 * mcap if pruned else 2 * n - 1
-        L, rad = _bluestein_len(lo, 6022)
-        if L < 0:
-            L, rad = _bluestein_len(lo, 12288)
-        if 0 < L <= 12288:
-            return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
-    rad = _pencils([p for p in primes if p <= 31]) + big
-    if not rad:
-        rad = [n]
-    return 3 * n * (len(rad) + (6 if big else 0)) + 16 * n + 32 * (mcap + 1)
+    small = [p for p in primes if p <= 16]
+    mid = [p for p in primes if 16 < p <= 127]
+    big = [p for p in primes if p > 127]
+    if not big and len(mid) <= 1:
+        rad = _pencils(small) + mid
+        if not rad:
+            rad = [n]
+        if len(rad) <= 4 and (not mid or len(rad) >= 2):
+            dp = mid[0] if mid else 0
+            return 3 * n * (len(rad) + dp // 16) + 16 * n + 32 * (mcap + 1)
+    # whole-ring Bluestein; even n keeping |k| <= mcap needs only n + 2 mcap lags
+    pruned = n % 2 == 0 and n + 2 * mcap < 2 * n - 1
+    lo = n + 2 * mcap if pruned else 2 * n - 1
+    L, rad = _bluestein_len(lo, 6022)
+    if L < 0:
+        L, rad = _bluestein_len(lo, 12288)
+    if 0 < L <= 12288:
+        return 3 * 2 * L * len(rad) + 16 * n + 32 * (mcap + 1)
+    rad = _pencils(small) + sorted(mid + big)
+    return 3 * n * (len(rad) + 6) + 16 * n + 32 * (mcap + 1)
 
 
 def ring_partition(nloen_north, mcap_north, P: int) -> np.ndarray:

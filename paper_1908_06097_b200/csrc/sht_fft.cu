@@ -17,7 +17,10 @@
 // registers and no second buffer is needed, so a 2576-point ring pair for one
 // field needs 82 KB and two CTAs share an SM.  The decimation-in-time
 // order leaves the spectrum digit-reversed (extraction reads it through
-// dit_pos).  A prime factor p > 31 of N becomes a Bluestein step (factor-local
+// dit_pos).  One prime factor 16 < p <= 127 becomes the last step, done as
+// FP64 tensor-core GEMMs (dmma_prime_step).  Larger primes (or two of them)
+// send the ring through whole-ring Bluestein (below), or, for rings too long
+// for one CTA, make a prime factor p > 16 a Bluestein step (factor-local
 // chirp-z): its DFT_p pencils are gathered G at a time into a work buffer,
 // convolved with the chirp kernel by an inner pencil FFT of 13-smooth length
 // Lp >= 2p-1 (DIT, kernel product fused into the last inner step, then the
@@ -163,6 +166,108 @@ __device__ __forceinline__ void step_dispatch(double2* buf, int nseq, int L, con
   }
 }
 
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// DMMA prime step: the DFT_p (p prime, 16 < p <= kMaxDmmaPrime) of every
+// contiguous pencil of the last DIT step as FP64 tensor-core GEMMs (SASS
+// DMMA.8x8x4), instead of padding the whole ring through Bluestein.  With
+// t_j = x_j + x_{p-j}, u_j = x_j - x_{p-j} (j = 1..H, H = (p-1)/2):
+//   A_k = sum_j cos(2 pi jk/p) t_j   (k = 0..H; A_0 = sum t_j),
+//   B_k = sum_j sin(2 pi jk/p) u_j,
+//   X_k = x_0 + A_k - i B_k,  X_{p-k} = x_0 + A_k + i B_k.
+// Each warp owns groups of 4 pencils (8 real columns = one DMMA n-tile): it
+// forms t/u in place, accumulates all (H+1) output rows of its group in
+// registers (<= 8 row tiles x {cos, sin}), then overwrites the group -- no
+// other warp touches those pencils, so a __syncwarp orders reads and writes.
+// A operand: (cos, sin)(2 pi ((k j) mod p) / p) from a p-entry table in shared
+// memory; B operand: t_j / u_j straight from the pencil.
+template <int V>
+__device__ void dmma_prime_step(double2* __restrict__ buf, int nseq, int L, const FftStep& st,
+                                const double2* __restrict__ cs) {
+  constexpr int NT = FftCfg<V>::kThreads;
+  constexpr int kTiles = (kMaxDmmaPrime - 1) / 2 / 8 + 1;  // row tiles of k = 0..H
+  const int p = st.R, H = (p - 1) >> 1;
+  const int npen = st.np;  // pencils per sequence (L / p)
+  const int tot = nseq * npen;
+  const int ngrp = (tot + 3) >> 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntile = (H + 8) >> 3;
+  const int nj = (H + 3) >> 2;
+  const uint32_t magp = (1u << 20) / (uint32_t)p + 1;  // (x * magp) >> 20 == x / p for x < 2^20 / p
+  auto pbase = [&](int pen) {                          // unpadded index of a pencil's point 0
+    const int q = fdiv(pen, st.mag_np);
+    return q * L + (pen - q * npen) * p;
+  };
+  for (int g = warp; g < ngrp; g += NT / 32) {
+    // 1. t / u in place: pairs (pencil, j) over the lanes
+    for (int idx = lane; idx < 4 * H; idx += 32) {
+      const int pl = idx / H, j = idx - pl * H + 1;
+      const int pen = 4 * g + pl;
+      if (pen < tot) {
+        const int b0 = pbase(pen);
+        const double2 a = buf[px(b0 + j)], b = buf[px(b0 + p - j)];
+        buf[px(b0 + j)] = cadd(a, b);
+        buf[px(b0 + p - j)] = csub(a, b);
+      }
+    }
+    __syncwarp();
+    // 2. GEMMs: rows k = 8 t + (lane >> 2), columns (pencil, re/im)
+    double acc[kTiles][2][2];
+#pragma unroll
+    for (int t = 0; t < kTiles; ++t) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
+    const int bpen = 4 * g + (lane >> 3), bre = (lane >> 2) & 1;  // B fragment: column lane >> 2
+    const bool bval = bpen < tot;
+    const int bb0 = bval ? pbase(bpen) : 0;
+    for (int js = 0; js < nj; ++js) {
+      const int j = 4 * js + (lane & 3) + 1;  // B row and A column of this lane
+      double bt = 0.0, bu = 0.0;
+      if (bval && j <= H) {
+        const double2 t = buf[px(bb0 + j)], u = buf[px(bb0 + p - j)];
+        bt = bre ? t.y : t.x;
+        bu = bre ? u.y : u.x;
+      }
+#pragma unroll
+      for (int t = 0; t < kTiles; ++t) {
+        if (t < ntile) {
+          const int k = 8 * t + (lane >> 2);
+          double ac = 0.0, as = 0.0;
+          if (j <= H && k <= H) {
+            const uint32_t x = (uint32_t)(k * j);
+            const double2 w = cs[x - ((x * magp) >> 20) * p];
+            ac = w.x;
+            as = w.y;
+          }
+          dmma(acc[t][0][0], acc[t][0][1], ac, bt);
+          dmma(acc[t][1][0], acc[t][1][1], as, bu);
+        }
+      }
+    }
+    // 3. outputs: this lane holds row k = 8 t + (lane >> 2) of pencil lane & 3
+    const int open = 4 * g + (lane & 3);
+    const bool oval = open < tot;
+    const int ob0 = oval ? pbase(open) : 0;
+    const double2 x0 = oval ? buf[px(ob0)] : make_double2(0.0, 0.0);
+    __syncwarp();  // every lane has read its t / u / x0
+    if (oval) {
+#pragma unroll
+      for (int t = 0; t < kTiles; ++t) {
+        const int k = 8 * t + (lane >> 2);
+        if (t < ntile && k <= H) {
+          const double ax = acc[t][0][0], ay = acc[t][0][1], bx = acc[t][1][0], by = acc[t][1][1];
+          buf[px(ob0 + k)] = make_double2(x0.x + ax + by, x0.y + ay - bx);
+          if (k) buf[px(ob0 + p - k)] = make_double2(x0.x + ax - by, x0.y + ay + bx);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // Bluestein step: every DFT_R pencil (R prime > 31) of the nseq sequences is
 // x -> w_k conj(conv(x w, conj w))_k, the convolution done by the inner pencil
 // FFT of length Lp on G pencils at a time in the work buffer W.
@@ -230,7 +335,9 @@ __device__ __forceinline__ void ring_dft(double2* buf, double2* W, int L, int ns
     return;
   }
   for (int j = 0; j < nstep; ++j) {
-    if (steps[j].blue)
+    if (steps[j].ptab >= 0)
+      dmma_prime_step<V>(buf, nseq, L, steps[j], twt + steps[j].ptab);
+    else if (steps[j].blue)
       bluestein_step<V>(buf, W, nseq, L, steps[j], j < nstep - 1, steps, twt, tab);
     else
       step_dispatch<V, true, false>(buf, nseq, L, steps[j], j < nstep - 1, twt, nullptr);
@@ -575,16 +682,13 @@ static void launch_one(bool g2f, const FftParams& p, int w0, int nw, const doubl
 void fft_preload() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, fft_g2f_kernel<1>);
-  cudaFuncGetAttributes(&a, fft_g2f_kernel<2>);
   cudaFuncGetAttributes(&a, fft_f2g_kernel<1>);
-  cudaFuncGetAttributes(&a, fft_f2g_kernel<2>);
 }
 
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s) {
   if (nw <= 0) return;
   if (variant == 1 || variant == 3) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
-  if (variant == 2) launch_one<2>(g2f, p, w0, nw, in, out, smem, s);
 }
 
 // ------------------------------------------------------------------ host-side planning
@@ -668,16 +772,32 @@ int fft_bluestein_len(int lo, std::vector<int>& radices, int lmax) {
 
 int fft_plan_ring(int n, RingPlan& rp, int mcap) {
   if (n < 2 || n > kFftMaxLen) return SHT_ERR_CONFIG;
-  std::vector<int> primes, small, big;
+  std::vector<int> primes, small, mid, big;
   factor_primes(n, n, primes);
-  for (int p : primes) (p > 31 ? big : small).push_back(p);
-  rp.bluestein = !big.empty();
+  for (int p : primes) (p <= 16 ? small : p <= kMaxDmmaPrime ? mid : big).push_back(p);
+  rp.variant = 1;
+  rp.dprime = 0;
   rp.ring_blue = false;
   rp.L = n;
   rp.wlen = 0;
   rp.mcap = -1;
   rp.shift = 0;
-  if (rp.bluestein) {  // whole-ring Bluestein when the padded transform fits one CTA
+  // direct: pencils <= 16 plus at most one prime 17..kMaxDmmaPrime as a DMMA
+  // prime step (last), <= kMaxSteps steps in all
+  if (big.empty() && mid.size() <= 1) {
+    group_pencils(small, rp.radices);
+    if (!mid.empty()) rp.radices.push_back(mid[0]);
+    if (rp.radices.empty()) rp.radices.push_back(n);
+    if ((int)rp.radices.size() <= kMaxSteps && (mid.empty() || rp.radices.size() >= 2)) {
+      rp.bluestein = false;
+      rp.dprime = mid.empty() ? 0 : mid[0];
+      return SHT_OK;
+    }
+  }
+  rp.bluestein = true;
+  for (int p : mid) big.push_back(p);
+  std::sort(big.begin(), big.end());
+  {  // whole-ring Bluestein when the padded transform fits one CTA
     // Chirp-z convolution between n points and the 2 mcap + 1 kept bins
     // spans n + 2 mcap lags (the chirp is n-periodic for even n), not 2n - 1.
     const bool pruned = mcap >= 0 && n % 2 == 0 && n + 2 * mcap < 2 * n - 1;
@@ -690,7 +810,6 @@ int fft_plan_ring(int n, RingPlan& rp, int mcap) {
       rp.ring_blue = true;
       rp.L = L;
       rp.radices = rad;
-      rp.variant = 1;
       if (pruned) {
         rp.mcap = mcap;
         rp.shift = L - n;
@@ -699,9 +818,6 @@ int fft_plan_ring(int n, RingPlan& rp, int mcap) {
     }
   }
   group_pencils(small, rp.radices);
-  rp.variant = 1;
-  for (int r : rp.radices)
-    if (r > 16) rp.variant = 2;
   int maxLp = 0;
   for (int p : big) {
     rp.radices.push_back(p);  // factor-local Bluestein steps last (contiguous pencils)
@@ -750,6 +866,7 @@ static FftStep make_step(int L, int B, int R, int tw_base) {
   st.mag_np = ((uint64_t)1 << 40) / (uint64_t)st.np + 1;
   st.mag_R = ((uint64_t)1 << 40) / (uint64_t)R + 1;
   st.chirp_off = st.bhat_off = -1;
+  st.ptab = -1;
   return st;
 }
 
@@ -814,7 +931,7 @@ int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps
   std::vector<std::pair<size_t, std::vector<int>>> blue_inner;  // ring-step index, inner radices
   for (size_t j = 0; j < ring.size(); ++j) {
     FftStep& st = ring[j];
-    if (st.R <= 31) continue;
+    if (st.R <= 16 || rp.dprime) continue;  // a direct plan's prime > 16 is its DMMA prime step
     std::vector<int> irad;
     const int Lp = fft_bluestein_len(2 * st.R - 1, irad, kFftMaxLen);
     const int base = (int)((int64_t)arena.size() - tw_off);
@@ -832,6 +949,15 @@ int fft_build_ring(int n, const RingPlan& rp, int G, std::vector<FftStep>& steps
       Bi /= Ri;
     }
     blue_inner.push_back({j, irad});
+  }
+  if (rp.dprime) {  // (cos, sin)(2 pi r / p) of the DMMA prime step, after the ring table
+    const int P = rp.dprime;
+    ring.back().ptab = (int)((int64_t)arena.size() - tw_off);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int r = 0; r < P; ++r) {
+      const long double a = two_pi * (long double)r / (long double)P;
+      arena.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+    }
   }
   ntw = (int)((int64_t)arena.size() - tw_off);
   if (ntw > kTwMax || ring.size() + inner.size() > (size_t)kMaxAllStepsHost) return SHT_ERR_CONFIG;

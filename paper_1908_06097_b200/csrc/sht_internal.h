@@ -104,7 +104,9 @@ struct FftStep {
   int32_t tw_base;     // offset of that transform's 2-level table (lo[64], hi[...]) in the ring table
   uint64_t mag_S, mag_np, mag_R;  // multiply-shift (>> 40) divisors
   // Bluestein step only (blue != 0)
-  int32_t blue, Lp, inner0, ninner, G, pad;
+  int32_t blue, Lp, inner0, ninner, G;
+  int32_t ptab;        // DMMA prime step (R prime, 17..kMaxDmmaPrime, last step): offset of the
+                       // (cos, sin)(2 pi r / R) table in the ring table; -1 otherwise
   uint64_t mag_Lp, mag_Rb;  // divisors by Lp and by R
   int64_t chirp_off;   // w_r = exp(-pi i r^2 / R), r < R
   int64_t bhat_off;    // inner-FFT spectrum of the chirp kernel / Lp, digit-reversed for the inner plan
@@ -160,9 +162,11 @@ void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const
 
 // Host plan of one ring length: steps (with Bluestein inner steps appended)
 // and the ring's twiddle / chirp tables appended to the arena.
+constexpr int kMaxDmmaPrime = 127;  // largest prime DFT done as FP64 tensor-core GEMMs (last step)
 struct RingPlan {
   int variant = 1;
-  bool bluestein = false;      // a prime factor > 31
+  int dprime = 0;              // a prime factor 17..kMaxDmmaPrime as a DMMA prime step (last step), else 0
+  bool bluestein = false;      // a prime factor > kMaxDmmaPrime, or two prime factors > 16
   bool ring_blue = false;      // whole-ring Bluestein (transform length L fits one CTA)
   int L = 0;                   // transform length
   int mcap = -1;               // pruned whole-ring Bluestein (even n): only |k| <= mcap is kept,

@@ -313,7 +313,9 @@ static int64_t ring_fft_cost(int n, int mcap) {
   RingPlan rp;
   if (fft_plan_ring(n, rp, mcap)) return 16LL * n;
   const int64_t ns = (int64_t)rp.radices.size();
-  const int64_t esteps = rp.ring_blue ? 2LL * rp.L * ns : (int64_t)n * (ns + (rp.bluestein ? 6 : 0));
+  // a DMMA prime step of p costs ~p/16 radix-16 steps; factor-local Bluestein ~6
+  const int64_t esteps = rp.ring_blue ? 2LL * rp.L * ns
+                                      : (int64_t)n * (ns + (rp.bluestein ? 6 : rp.dprime / 16));
   return 3 * esteps + 16LL * n + 32LL * (mcap + 1);
 }
 
@@ -797,7 +799,8 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     R.wlen = Lp * std::max(G, 1);
     p->fft_smem[variant] = std::max(p->fft_smem[variant], smem(nb, G));
     const int64_t esteps = rp.ring_blue ? 2LL * R.L * (int64_t)rp.radices.size()
-                                        : (int64_t)R.n * ((int64_t)rp.radices.size() + (rp.bluestein ? 6 : 0));
+                                        : (int64_t)R.n * ((int64_t)rp.radices.size() +
+                                                          (rp.bluestein ? 6 : rp.dprime / 16));
     ring_cost[lr] = (int64_t)nfld * (esteps + 4LL * R.n);
   }
   // split every ring's fields over CTAs so each variant's launch has

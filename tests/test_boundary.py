@@ -117,8 +117,8 @@ def test_bluestein_length_matches_restatement(lib):
     for n in range(20, 2600, 4):
         info = fft_plan_info(n)            # no pruning: |k| <= n/2 kept
         primes, _ = _factor(n, n)
-        if not any(p > 31 for p in primes):
-            continue
+        if not (any(p > 127 for p in primes) or sum(p > 16 for p in primes) >= 2):
+            continue                       # direct, possibly with a DMMA prime step
         L, rad = _bluestein_len(2 * n - 1, 6022)
         if L < 0:
             L, rad = _bluestein_len(2 * n - 1, 12288)
@@ -134,7 +134,11 @@ def test_fft_plans(lib):
     p20 = fft_plan_info(20)
     assert p20["length"] == 20 and not p20["bluestein"] and len(p20["radices"]) == 2
     assert len(fft_plan_info(2560)["radices"]) == 3                 # 16 x 16 x 10
-    assert not fft_plan_info(2576)["bluestein"]                     # 2^4 * 7 * 23: direct radix-23 step
+    assert not fft_plan_info(2576)["bluestein"]                     # 2^4 * 7 * 23: direct, DMMA prime-23 step
+    assert fft_plan_info(2576)["radices"][-1] == 23
+    p508 = fft_plan_info(508)                                       # 4 * 127: the largest DMMA prime step
+    assert not p508["bluestein"] and p508["radices"] == [4, 127]
+
     big = fft_plan_info(2572)                                       # 4 * 643: whole-ring Bluestein
     assert big["bluestein"] and big["length"] >= 2 * 2572 - 1
     assert fft_plan_info(8016)["radices"][-1] == 167                # factor-local Bluestein step (TCo1999)
@@ -145,8 +149,9 @@ def test_fft_plans(lib):
         assert int(np.prod(info["radices"])) == info["length"]
         if info["length"] != n:                                     # whole-ring Bluestein
             assert info["bluestein"] and info["length"] >= 2 * n - 1
-        else:
-            assert info["bluestein"] == any(r > 31 for r in info["radices"])
+        elif not info["bluestein"]:                                 # direct: <= one DMMA prime step, last
+            big = [r for r in info["radices"] if r > 16]
+            assert len(big) <= 1 and all(r <= 127 for r in big) and (not big or info["radices"][-1] == big[0])
 
 
 def test_errors_map_to_reference_classes(lib):
