@@ -9,11 +9,14 @@ anything on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import ConfigurationError, ProtocolError
 
-LIB_PATH = Path(__file__).resolve().parent / "libsht.so"
+# SHT_LIB overrides the library for A/B timing of two builds (tools/); the
+# default is the in-tree build
+LIB_PATH = Path(os.environ.get("SHT_LIB") or Path(__file__).resolve().parent / "libsht.so")
 
 SHT_OK = 0
 SHT_ERR_CONFIG = 1

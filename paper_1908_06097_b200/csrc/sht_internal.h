@@ -18,10 +18,12 @@ namespace sht {
 __device__ __forceinline__ void st_slot(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
+// (not volatile, no memory clobber: a read of data no kernel writes while it
+// runs, so the compiler may batch several of them before their first use)
 __device__ __forceinline__ void ld_slot(const double* p, double& a, double& b, double& c, double& d) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
-               : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p));
 }
 #endif
 
