@@ -467,39 +467,70 @@ __device__ __forceinline__ double eps_nm(int n, int m) {
 
 // One thread per (local m, ring): three-term recurrence in n on the mantissa,
 // shared per-ring exponent, renormalised by 2^-400 above 2^400.
-__global__ void leg_poly_kernel(int T, int nh, int lm0, const int32_t* __restrict__ lm_m, const int32_t* __restrict__ lm_i0,
-                                const int64_t* __restrict__ lm_poff, const int32_t* __restrict__ lm_kp,
-                                const double* __restrict__ mu, const double* __restrict__ dmant,
-                                const int32_t* __restrict__ dexp, double* __restrict__ ptab) {
+// A warp's 32 rings produce 32 columns n at a time into a shared-memory tile,
+// which the warp then stores row by row (one coalesced 256-byte segment per
+// ring) -- a thread writing its own row (stride Kp) made every store
+// instruction touch 32 rows.  eps(n, m) (a division and a square root) is the
+// same for every ring: lane L computes it for column c0 + L of the chunk and
+// the warp shares it by shuffles, instead of every ring recomputing it.  The
+// arithmetic and its order are unchanged, so the table stays bit-identical to
+// the oracle's.
+constexpr int kPolyThreads = 128;
+__global__ void __launch_bounds__(kPolyThreads)
+    leg_poly_kernel(int T, int nh, int lm0, const int32_t* __restrict__ lm_m, const int32_t* __restrict__ lm_i0,
+                    const int64_t* __restrict__ lm_poff, const int32_t* __restrict__ lm_kp,
+                    const double* __restrict__ mu, const double* __restrict__ dmant, const int32_t* __restrict__ dexp,
+                    double* __restrict__ ptab) {
+  __shared__ double tile[kPolyThreads / 32][32][33];
   const int lm = lm0 + blockIdx.y;
   const int m = lm_m[lm];
   const int i0 = lm_i0[lm];
-  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nh) return;
-  const int kp = lm_kp[lm];
-  double* out = ptab + lm_poff[lm] + (int64_t)(i - i0) * kp;
-  const double x = mu[i];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int ring0 = i0 + blockIdx.x * kPolyThreads + wp * 32;  // first ring of this warp
+  if (ring0 >= nh) return;
+  const int i = ring0 + lane;
+  const bool live = i < nh;
+  const int kp = lm_kp[lm], K = T - m + 1;
+  double* rows = ptab + lm_poff[lm] + (int64_t)(ring0 - i0) * kp;
+  const int nrow = min(32, nh - ring0);
+  const double x = live ? mu[i] : 0.0;
   const double two400 = 0x1p400, twom400 = 0x1p-400;
-  int e = dexp[(int64_t)lm * nh + i];
-  double q2 = dmant[(int64_t)lm * nh + i];
-  for (int n = T - m + 1; n < kp; ++n) out[n] = 0.0;  // zero padding (the scratch is reused in recompute mode)
-  out[0] = ldexp(q2, e);
-  if (m == T) return;
-  double q1 = __dmul_rn(__dmul_rn(sqrt(2.0 * m + 3.0), x), q2);
-  out[1] = ldexp(q1, e);
-  double epsm1 = eps_nm(m + 1, m);
-  for (int n = m + 2; n <= T; ++n) {
-    const double epsn = eps_nm(n, m);
-    double q = __ddiv_rn(__dsub_rn(__dmul_rn(x, q1), __dmul_rn(epsm1, q2)), epsn);
-    if (fabs(q) > two400) {
-      q = __dmul_rn(q, twom400);
-      q1 = __dmul_rn(q1, twom400);
-      e += 400;
+  int e = live ? dexp[(int64_t)lm * nh + i] : 0;
+  double q2 = live ? dmant[(int64_t)lm * nh + i] : 0.0;
+  double q1 = 0.0, epsm1 = 0.0;
+  double (*tl)[33] = tile[wp];
+  for (int c0 = 0; c0 < kp; c0 += 32) {
+    const double eps_l = (c0 + lane >= 1 && c0 + lane < K) ? eps_nm(m + c0 + lane, m) : 0.0;  // column c0 + lane
+    for (int cc = 0; cc < 32; ++cc) {  // column c = n - m of this lane's ring
+      const int c = c0 + cc;
+      const double eps_c = __shfl_sync(0xffffffffu, eps_l, cc);
+      double v = 0.0;  // zero padding beyond K (the scratch is reused in recompute mode)
+      if (c == 0) {
+        v = ldexp(q2, e);
+      } else if (c == 1 && c < K) {
+        q1 = __dmul_rn(__dmul_rn(sqrt(2.0 * m + 3.0), x), q2);
+        epsm1 = eps_c;  // eps(m + 1, m)
+        v = ldexp(q1, e);
+      } else if (c < K) {
+        const double epsn = eps_c;  // eps(m + c, m)
+        double q = __ddiv_rn(__dsub_rn(__dmul_rn(x, q1), __dmul_rn(epsm1, q2)), epsn);
+        if (fabs(q) > two400) {
+          q = __dmul_rn(q, twom400);
+          q1 = __dmul_rn(q1, twom400);
+          e += 400;
+        }
+        q2 = q1;
+        q1 = q;
+        epsm1 = epsn;
+        v = ldexp(q, e);
+      }
+      tl[lane][cc] = v;
     }
-    q2 = q1;
-    q1 = q;
-    epsm1 = epsn;
-    out[n - m] = ldexp(q, e);
+    __syncwarp();
+    const int ncol = min(32, kp - c0);
+    if (lane < ncol)
+      for (int r = 0; r < nrow; ++r) rows[(int64_t)r * kp + c0 + lane] = tl[r][lane];
+    __syncwarp();
   }
 }
 
@@ -550,8 +581,8 @@ void launch_leg_poly(int T, int nh, int lm0, int lm1, const int32_t* lm_m, const
                      const int64_t* lm_poff, const int32_t* lm_kp, const double* mu, const double* dmant,
                      const int32_t* dexp, double* ptab, cudaStream_t s) {
   if (lm1 <= lm0) return;
-  dim3 grid((nh + 127) / 128, lm1 - lm0);
-  leg_poly_kernel<<<grid, 128, 0, s>>>(T, nh, lm0, lm_m, lm_i0, lm_poff, lm_kp, mu, dmant, dexp, ptab);
+  dim3 grid((nh + kPolyThreads - 1) / kPolyThreads, lm1 - lm0);
+  leg_poly_kernel<<<grid, kPolyThreads, 0, s>>>(T, nh, lm0, lm_m, lm_i0, lm_poff, lm_kp, mu, dmant, dexp, ptab);
 }
 
 }  // namespace sht
