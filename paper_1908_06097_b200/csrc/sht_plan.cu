@@ -352,6 +352,7 @@ static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, 
 
 // ------------------------------------------------------------------ transposition
 enum FlagSlot { kYArr = 0, kXArr = 1, kYFree = 2, kXFree = 3 };
+constexpr double kP2PMaxBytes = 8.0 * (1 << 30);  // largest receive buffer the p2p transport stores into
 
 // Handshake of the p2p transposition, one thread per peer t: publish
 // `sig_v` in slot `sig_slot` of peer t's flag words (release, system scope:
@@ -532,8 +533,18 @@ static int build_transport(sht_plan* p) {
   p->peer_x[r] = p->X;
   p->peer_y[r] = p->Y;
   if (P > 1) {
+    // p2p unless SHT_TRANSPORT=nccl, or (without SHT_TRANSPORT=p2p) the
+    // receive buffers the kernels would store into over NVLink are large and
+    // spread over >= 2 peers, where the scattered remote row stores fall off
+    // a translation cliff: at TCo1999 x 548 on 4 B200 (13 GB per rank) the
+    // fused fft_g2f took 120 ms against 49 ms with local stores + NCCL, while
+    // 13 GB on 2 B200 and 6.6 GB on 4 B200 showed no cliff
+    // (profiles/r02_transport_cliff.md)
     const char* tr = getenv("SHT_TRANSPORT");
-    const bool want = !(tr && std::string(tr) == "nccl");
+    const double rbuf = (double)std::max(p->xtot, p->ytot) * (double)p->nfld * 32.0;
+    const bool force_p2p = tr && std::string(tr) == "p2p";
+    const bool cliff = P >= 3 && rbuf > kP2PMaxBytes;
+    const bool want = !(tr && std::string(tr) == "nccl") && (force_p2p || !cliff);
     SHT_CUDA_TRY(cudaMalloc((void**)&p->flagw, 4 * P * sizeof(uint32_t)));
     SHT_CUDA_TRY(cudaMemset(p->flagw, 0, 4 * P * sizeof(uint32_t)));
     p->peer_flags[r] = p->flagw;
