@@ -169,6 +169,42 @@ int sht_alltoall_order(int nranks, int rank, int32_t* peers);
  * whether Bluestein is used. */
 int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein);
 
+/* ---- GPU halo engine: the reference's unstructured-grid
+ * halo exchange and neighbourhood-mean stencil on device-resident fields ---- */
+typedef struct sht_halo sht_halo;
+
+/* One rank's exchange plan -- the reference's RankPlan (halo/plan.py:33-55):
+ * send_counts[p] local owned indices to gather for peer p (send_index, peers
+ * ascending, each list ascending in global order), recv_counts[p] ghost slots
+ * the matching buffer from p scatters into (recv_slot).  The local array is
+ * the owned elements then the ghosts (halo/partition.py:1-6).  Optional
+ * stencil: ngroups degree groups (engine._stencil_ws), group g has
+ * group_count[g] owned members and a [count][degree] row-major table of
+ * their neighbours' local indices (ascending global order per row).
+ * nccl_unique_id as for sht_plan_create (NULL when nranks == 1).  Collective.
+ * Errors: SHT_ERR_CONFIG for an out-of-range plan (the reference raises
+ * ProtocolError / ConfigurationError, plan.py:106-120, engine.py:126-139). */
+int sht_halo_create(int rank, int nranks, const void* nccl_unique_id, int64_t n_local, int64_t n_owned,
+                    const int64_t* send_counts, const int64_t* send_index, const int64_t* recv_counts,
+                    const int64_t* recv_slot, int ngroups, const int32_t* group_degree, const int64_t* group_count,
+                    const int64_t* members, const int64_t* neighbours, sht_halo** out);
+
+/* Replaces engine.exchange (engine.py:197-220): refresh every ghost of
+ * `values` (device, n_local doubles) with its owner's value -- pack, grouped
+ * send/recv in the ROTATED_CONCURRENT order (engine.py:146-149), unpack.
+ * Stream-ordered; bounded by SHT_COMM_TIMEOUT_MS on a dead peer. */
+int sht_halo_exchange(sht_halo* halo, double* values, void* cuda_stream);
+
+/* Replaces engine.stencil_step with OverlapMode.NONE (engine.py:301-327):
+ * exchange, then owned[m] = mean of values[neighbours of m], accumulated in
+ * the reference's order (bit-identical). */
+int sht_halo_stencil_step(sht_halo* halo, double* values, void* cuda_stream);
+
+/* Elements this rank sends / receives per exchange. */
+int sht_halo_counts(const sht_halo* halo, int64_t* nsend, int64_t* nrecv);
+
+void sht_halo_destroy(sht_halo* halo);
+
 #ifdef __cplusplus
 }
 #endif
