@@ -169,6 +169,31 @@ int sht_alltoall_order(int nranks, int rank, int32_t* peers);
  * whether Bluestein is used. */
 int sht_fft_plan_info(int n, int32_t* radices, int32_t* nstages, int32_t* fft_len, int32_t* bluestein);
 
+/* ---- 2-D grid-point layout: latitude bands x longitude
+ * segments, and the second (TRGTOL / TRLTOG-style [domain: ecTrans]) transposition
+ * between it and the ring-pair distribution of the FFTs ---- */
+
+/* Use an nA x nB grid-point layout (nA * nB == nranks): rank a*nB + b holds, per
+ * field, the points k in [floor(N_j b / nB), floor(N_j (b+1) / nB)) of every
+ * ring j of latitude band a (contiguous global rings, north first, split where
+ * the cumulative point count crosses a/nA of the total), rings ascending.
+ * Allocates the plan's transposition buffers.  Call on every rank. */
+int sht_plan_set_gp_layout(sht_plan* plan, int nA, int nB);
+
+/* This rank's grid-point layout: points per field, its band's global rings
+ * [band_lo, band_hi), its segment and the number of segments. */
+int sht_gp_layout(const sht_plan* plan, int64_t* npts_gp, int32_t* band_lo, int32_t* band_hi, int32_t* segment,
+                  int32_t* nsegments);
+
+/* inv_trans / dir_trans with the grid in the grid-point layout
+ * ([nfld][npts_gp] device buffers): the ring-pair transform plus the
+ * ring <-> grid-point transposition (grouped NCCL send/recv, rotated order). */
+int sht_inv_trans_gp(sht_plan* plan, const double* spec, double* grid_gp, void* cuda_stream);
+int sht_dir_trans_gp(sht_plan* plan, const double* grid_gp, double* spec, void* cuda_stream);
+
+/* Host-only: first global ring of each of the nA latitude bands (+ NDGL): band_lo[nA + 1]. */
+int sht_gp_bands(int truncation, int ndgl, const int32_t* nloen, int nA, int32_t* band_lo);
+
 /* ---- GPU halo engine: the reference's unstructured-grid
  * halo exchange and neighbourhood-mean stencil on device-resident fields ---- */
 typedef struct sht_halo sht_halo;

@@ -224,3 +224,37 @@ def emulate_inv(o: SHTransformOracle, spec: np.ndarray, P: int):
     lay = Layout(o, P)
     send = [lay.pack_inv(lay.local_spec(spec, r), r) for r in range(P)]
     return [lay.unpack_inv([send[s][r] for s in range(P)], r) for r in range(P)], lay
+
+
+# ------------------------------------------------------------------ 2-D grid-point layout
+def gp_bands(nloen, nA: int):
+    """First global ring of every latitude band (+ NDGL): contiguous rings, split where the
+    cumulative point count crosses a / nA of the total (libsht's gp_bands)."""
+    nloen = [int(n) for n in nloen]
+    tot = sum(nloen)
+    lo = [len(nloen)] * (nA + 1)
+    lo[0] = 0
+    cum, a = 0, 1
+    for j, n in enumerate(nloen):
+        if a >= nA:
+            break
+        cum += n
+        while a < nA and cum * nA >= tot * a:
+            lo[a] = j + 1
+            a += 1
+    return lo
+
+
+def gp_local(grid: np.ndarray, nloen, rank: int, nA: int, nB: int) -> np.ndarray:
+    """Rank a nB + b's grid-point-layout slice of a global grid [nfld, NPTS]: segment b
+    (points [floor(N_j b / nB), floor(N_j (b+1) / nB))) of every ring j of band a."""
+    nloen = np.asarray(nloen, dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(nloen)])
+    lo = gp_bands(nloen, nA)
+    a, b = rank // nB, rank % nB
+    cols = []
+    for j in range(lo[a], lo[a + 1]):
+        k0, k1 = nloen[j] * b // nB, nloen[j] * (b + 1) // nB
+        cols.append(np.arange(off[j] + k0, off[j] + k1))
+    idx = np.concatenate(cols) if cols else np.zeros(0, dtype=np.int64)
+    return grid[:, idx]

@@ -19,7 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsht.so"
 OBJ = ROOT / "build" / "obj"
-SOURCES = ["sht_plan.cu", "sht_legendre.cu", "sht_fft.cu", "sht_halo.cu"]
+SOURCES = ["sht_plan.cu", "sht_legendre.cu", "sht_fft.cu", "sht_halo.cu", "sht_gp.cu"]
 HEADERS = ["sht_internal.h", "fft_codelets.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

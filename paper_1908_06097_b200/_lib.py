@@ -30,6 +30,7 @@ EXPORTS = (
     "sht_version", "sht_plan_create", "sht_inv_trans", "sht_dir_trans", "sht_local_layout",
     "sht_phase_ms", "sht_phase_ms_avg", "sht_work", "sht_kernel_launches", "sht_transport", "sht_nccl_get_unique_id", "sht_plan_destroy", "sht_plan_close", "sht_wait", "sht_last_error",
     "sht_plan_validate", "sht_gauss_nodes", "sht_partition", "sht_alltoall_rows", "sht_alltoall_order", "sht_fft_plan_info",
+    "sht_plan_set_gp_layout", "sht_gp_layout", "sht_inv_trans_gp", "sht_dir_trans_gp", "sht_gp_bands",
     "sht_halo_create", "sht_halo_exchange", "sht_halo_stencil_step", "sht_halo_counts", "sht_halo_destroy",
 )
 
@@ -75,6 +76,11 @@ def load() -> C.CDLL:
     lib.sht_alltoall_rows.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i64p]
     lib.sht_alltoall_order.argtypes = [C.c_int, C.c_int, i32p]
     lib.sht_fft_plan_info.argtypes = [C.c_int, i32p, i32p, i32p, i32p]
+    lib.sht_plan_set_gp_layout.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    lib.sht_gp_layout.argtypes = [C.c_void_p, i64p, i32p, i32p, i32p, i32p]
+    lib.sht_inv_trans_gp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.sht_dir_trans_gp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.sht_gp_bands.argtypes = [C.c_int, C.c_int, i32p, C.c_int, i32p]
     lib.sht_halo_create.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64, i64p, i64p, i64p, i64p,
                                     C.c_int, i32p, i64p, i64p, i64p, C.POINTER(C.c_void_p)]
     lib.sht_halo_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]

@@ -190,4 +190,23 @@ __host__ __device__ inline size_t fft_slots(size_t n) { return n + n / 16 + 1; }
 // Smallest 13-smooth length >= lo whose pencil plan has <= kMaxSteps steps.
 int fft_bluestein_len(int lo, std::vector<int>& radices, int lmax);
 
+// ---------------------------------------------------------------- 2-D grid-point layout (sht_gp.cu)
+struct GpLayout {
+  int nA = 0, nB = 0;                  // latitude bands x longitude segments (0: not set)
+  std::vector<int> band_lo;            // [nA + 1] first global ring of every band
+  int64_t npts_gp = 0;                 // grid-point-layout points of this rank per field
+  std::vector<int32_t> send_idx;       // ring layout -> GP: my ring-layout index per point, by destination
+  std::vector<int64_t> send_displ;     // [P + 1]
+  std::vector<int32_t> recv_idx;       // my GP-layout index per incoming point, by source
+  std::vector<int64_t> recv_displ;     // [P + 1]
+};
+void gp_bands(const std::vector<int>& nloen, int nA, std::vector<int>& band_lo);
+int gp_build(const std::vector<int>& nloen, const std::vector<int>& ring_rank, int P, int rank, int nA, int nB,
+             GpLayout& L);
+void gp_launch_pack(const double* src, int64_t src_ld, const int32_t* idx, const int64_t* displ, int P, int64_t ntot,
+                    int nfld, double* buf, cudaStream_t s);
+void gp_launch_unpack(const double* buf, const int32_t* idx, const int64_t* displ, int P, int64_t ntot, int nfld,
+                      double* dst, int64_t dst_ld, cudaStream_t s);
+void gp_preload();
+
 }  // namespace sht

@@ -252,6 +252,11 @@ struct sht_plan {
   double** d_ring_out = nullptr;                // [nh] leg_inv destination row of (ring, lm = 0)
   double** d_rows_out = nullptr;                // fft_g2f destination row per (local ring, m)
   const double** d_rows_in = nullptr;           // fft_f2g source row per (local ring, m)
+  // 2-D grid-point layout (sht_plan_set_gp_layout): the TRGTOL-style transposition
+  sht::GpLayout gp;
+  int32_t *d_gp_send_idx = nullptr, *d_gp_recv_idx = nullptr;
+  int64_t *d_gp_send_displ = nullptr, *d_gp_recv_displ = nullptr;
+  double *d_gridR = nullptr, *d_gp_buf0 = nullptr, *d_gp_buf1 = nullptr;
   // failure detection (nranks > 1): handshake error word in mapped host memory
   int32_t* h_err = nullptr;
   int32_t* d_err = nullptr;
@@ -279,7 +284,8 @@ static void free_plan(sht_plan* p) {
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
                   p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->flagw, p->d_peer_flags,
-                  p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in};
+                  p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in, p->d_gp_send_idx, p->d_gp_recv_idx,
+                  p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_events) {
@@ -858,6 +864,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   fft_preload();
   leg_preload();
   flag_preload();
+  gp_preload();
   int dev = 0;
   SHT_CUDA_TRY(cudaGetDevice(&dev));
   SHT_CUDA_TRY(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1305,6 +1312,120 @@ int sht_dir_trans(sht_plan* p, const double* grid, double* spec, void* stream) {
   if (p->p2p)
     if (int rc = flags_op(p, kXFree, e, -1, 0, s)) return rc;
   hist_advance(p, false);
+  return SHT_OK;
+}
+
+int sht_plan_set_gp_layout(sht_plan* p, int nA, int nB) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (nA < 1 || nB < 1 || nA * nB != p->nranks)
+    return fail(SHT_ERR_CONFIG, "grid-point layout needs nA * nB == nranks");
+  if (nA > p->g.ndgl) return fail(SHT_ERR_CONFIG, "more latitude bands than rings");
+  for (int n : p->g.nloen)
+    if (n < nB) return fail(SHT_ERR_CONFIG, "a ring has fewer points than longitude segments");
+  if (p->gp.nA) return fail(SHT_ERR_CONFIG, "the grid-point layout is already set");
+  std::vector<int> ring_rank(p->g.ndgl);
+  for (int j = 0; j < p->g.ndgl; ++j) ring_rank[j] = p->ring_owner[std::min(j, p->g.ndgl - 1 - j)];
+  if (gp_build(p->g.nloen, ring_rank, p->nranks, p->rank, nA, nB, p->gp))
+    return fail(SHT_ERR_CONFIG, "grid-point layout too large");
+  const size_t nf = (size_t)p->nfld;
+  if (int rc = upload(&p->d_gp_send_idx, p->gp.send_idx)) return rc;
+  if (int rc = upload(&p->d_gp_recv_idx, p->gp.recv_idx)) return rc;
+  if (int rc = upload(&p->d_gp_send_displ, p->gp.send_displ)) return rc;
+  if (int rc = upload(&p->d_gp_recv_displ, p->gp.recv_displ)) return rc;
+  const size_t nb = std::max<size_t>(1, std::max(p->gp.send_idx.size(), p->gp.recv_idx.size())) * nf;
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_gridR, std::max<int64_t>(p->grid_ld, 1) * nf * sizeof(double)));
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_gp_buf0, nb * sizeof(double)));
+  SHT_CUDA_TRY(cudaMalloc((void**)&p->d_gp_buf1, nb * sizeof(double)));
+  return SHT_OK;
+}
+
+int sht_gp_layout(const sht_plan* p, int64_t* npts_gp, int32_t* band_lo, int32_t* band_hi, int32_t* segment,
+                  int32_t* nsegments) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (!p->gp.nA) return fail(SHT_ERR_CONFIG, "no grid-point layout set (sht_plan_set_gp_layout)");
+  const int a = p->rank / p->gp.nB, b = p->rank % p->gp.nB;
+  if (npts_gp) *npts_gp = p->gp.npts_gp;
+  if (band_lo) *band_lo = p->gp.band_lo[a];
+  if (band_hi) *band_hi = p->gp.band_lo[a + 1];
+  if (segment) *segment = b;
+  if (nsegments) *nsegments = p->gp.nB;
+  return SHT_OK;
+}
+
+}  // extern "C"
+
+namespace sht {
+// Grouped send/recv of [peer block][field][point] buffers in the rotated
+// order (collectives.py:85-86); the self block is a device copy.
+static int gp_exchange(sht_plan* p, const double* sbuf, const std::vector<int64_t>& sdispl, double* rbuf,
+                       const std::vector<int64_t>& rdispl, cudaStream_t s) {
+  const int P = p->nranks, r = p->rank;
+  const int64_t nf = p->nfld;
+  const int64_t self = sdispl[r + 1] - sdispl[r];
+  if (self != rdispl[r + 1] - rdispl[r]) return fail(SHT_ERR_CONFIG, "grid-point layout self block mismatch");
+  if (self)
+    SHT_CUDA_TRY(cudaMemcpyAsync(rbuf + rdispl[r] * nf, sbuf + sdispl[r] * nf, self * nf * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+  if (P == 1) return SHT_OK;
+  if (p->failed || !p->comm) return comm_check(p);
+  SHT_NCCL_TRY(ncclGroupStart());
+  for (int k = 1; k < P; ++k) {
+    const int to = (r + k) % P, from = (r - k + P) % P;
+    const int64_t ns = sdispl[to + 1] - sdispl[to], nr = rdispl[from + 1] - rdispl[from];
+    if (ns) SHT_NCCL_TRY(ncclSend(sbuf + sdispl[to] * nf, (size_t)(ns * nf), ncclDouble, to, p->comm, s));
+    if (nr) SHT_NCCL_TRY(ncclRecv(rbuf + rdispl[from] * nf, (size_t)(nr * nf), ncclDouble, from, p->comm, s));
+  }
+  return nccl_settle(p, ncclGroupEnd(), "ncclGroupEnd (grid-point transposition)");
+}
+}  // namespace sht
+
+extern "C" {
+
+// inv_trans with the grid in the 2-D grid-point layout: the ring-pair grid
+// goes through the plan's buffer, then ring -> grid point (TRLTOG role).
+int sht_inv_trans_gp(sht_plan* p, const double* spec, double* grid_gp, void* stream) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (!p->gp.nA) return fail(SHT_ERR_CONFIG, "no grid-point layout set (sht_plan_set_gp_layout)");
+  if (int rc = check_ptr(grid_gp, "grid")) return rc;
+  if (p->nranks == 1) return sht_inv_trans(p, spec, grid_gp, stream);  // 1 x 1 layout == ring layout
+  if (int rc = sht_inv_trans(p, spec, p->d_gridR, stream)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const GpLayout& L = p->gp;
+  gp_launch_pack(p->d_gridR, p->grid_ld, p->d_gp_send_idx, p->d_gp_send_displ, p->nranks,
+                 (int64_t)L.send_idx.size(), p->nfld, p->d_gp_buf0, s);
+  if (int rc = gp_exchange(p, p->d_gp_buf0, L.send_displ, p->d_gp_buf1, L.recv_displ, s)) return rc;
+  gp_launch_unpack(p->d_gp_buf1, p->d_gp_recv_idx, p->d_gp_recv_displ, p->nranks, (int64_t)L.recv_idx.size(),
+                   p->nfld, grid_gp, L.npts_gp, s);
+  SHT_CUDA_TRY(cudaGetLastError());
+  return SHT_OK;
+}
+
+// dir_trans from the 2-D grid-point layout: grid point -> ring (TRGTOL role),
+// then the ring-pair transform.
+int sht_dir_trans_gp(sht_plan* p, const double* grid_gp, double* spec, void* stream) {
+  if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
+  if (!p->gp.nA) return fail(SHT_ERR_CONFIG, "no grid-point layout set (sht_plan_set_gp_layout)");
+  if (int rc = check_ptr(grid_gp, "grid")) return rc;
+  if (p->nranks == 1) return sht_dir_trans(p, grid_gp, spec, stream);
+  if (int rc = comm_check(p)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const GpLayout& L = p->gp;
+  gp_launch_pack(grid_gp, L.npts_gp, p->d_gp_recv_idx, p->d_gp_recv_displ, p->nranks, (int64_t)L.recv_idx.size(),
+                 p->nfld, p->d_gp_buf1, s);
+  if (int rc = gp_exchange(p, p->d_gp_buf1, L.recv_displ, p->d_gp_buf0, L.send_displ, s)) return rc;
+  gp_launch_unpack(p->d_gp_buf0, p->d_gp_send_idx, p->d_gp_send_displ, p->nranks, (int64_t)L.send_idx.size(),
+                   p->nfld, p->d_gridR, p->grid_ld, s);
+  SHT_CUDA_TRY(cudaGetLastError());
+  return sht_dir_trans(p, p->d_gridR, spec, stream);
+}
+
+int sht_gp_bands(int truncation, int ndgl, const int32_t* nloen, int nA, int32_t* band_lo) {
+  Geometry g;
+  if (int rc = make_geometry(truncation, ndgl, nloen, g)) return rc;
+  if (nA < 1 || nA > g.ndgl) return fail(SHT_ERR_CONFIG, "invalid number of latitude bands");
+  std::vector<int> b;
+  gp_bands(g.nloen, nA, b);
+  if (band_lo) std::copy(b.begin(), b.end(), band_lo);
   return SHT_OK;
 }
 

@@ -59,10 +59,14 @@ class SHTransform:
                  chunk of wavenumbers (bounded 2 GB scratch) right before the
                  GEMM tiles that use it, every transform (TCo1999 memory mode).
     profile    : record CUDA events around every phase (see ``phase_ms``).
+    gp_layout  : (nA, nB) with nA * nB = ranks: the grid side in a 2-D grid-point
+                 layout (nA latitude bands x nB longitude segments, see
+                 ``local_layout``) instead of whole ring pairs; inv_trans / dir_trans
+                 then add the ring <-> grid-point transposition (TRGTOL / TRLTOG role).
     """
 
     def __init__(self, truncation: int, grid="octahedral", nfld: int = 1, *, group=None,
-                 recompute_legendre: bool = False, profile: bool = False, device=None):
+                 recompute_legendre: bool = False, profile: bool = False, device=None, gp_layout=None):
         import torch
 
         lib = _lib.load()
@@ -129,11 +133,29 @@ class SHTransform:
         self.npts_local = int(npts.value)
         self.m_list = np.array(mlist[: nm.value], dtype=np.int64)
         self.ring_list = np.array(rlist[: nr.value], dtype=np.int64)
+        self.gp = None
+        if gp_layout is not None:
+            nA, nB = (int(x) for x in gp_layout)
+            with torch.cuda.device(self.device):
+                _lib.check(lib.sht_plan_set_gp_layout(plan, nA, nB))
+            npg, lo, hi, seg, nseg = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            _lib.check(lib.sht_gp_layout(plan, C.byref(npg), C.byref(lo), C.byref(hi), C.byref(seg), C.byref(nseg)))
+            self.gp = {"nA": nA, "nB": nB, "npts_gp_local": int(npg.value), "band_rings": (lo.value, hi.value),
+                       "segment": seg.value, "nsegments": nseg.value}
+            self.npts_grid = int(npg.value)
+        else:
+            self.npts_grid = self.npts_local
 
     # ------------------------------------------------------------------ helpers
     def local_layout(self) -> dict:
-        return {"nspec_local": self.nspec_local, "npts_local": self.npts_local,
-                "m_list": self.m_list.copy(), "ring_list": self.ring_list.copy()}
+        """This rank's spectral wavenumbers and ring pairs; with a grid-point layout also its
+        latitude band (global rings [lo, hi)) and longitude segment (points
+        [floor(N_j s / nB), floor(N_j (s+1) / nB)) of each ring)."""
+        out = {"nspec_local": self.nspec_local, "npts_local": self.npts_local,
+               "m_list": self.m_list.copy(), "ring_list": self.ring_list.copy()}
+        if self.gp:
+            out["gp"] = dict(self.gp)
+        return out
 
     def work(self) -> dict:
         """Algorithmic work of this rank per inverse+direct pair."""
@@ -232,11 +254,13 @@ class SHTransform:
         on ``stream`` / the current stream) or a host numpy array (copied in and
         the result copied back to a numpy array).
         """
-        return self._run(self._lib.sht_inv_trans, spec, self.nspec_local, self.npts_local, out, stream)
+        fn = self._lib.sht_inv_trans_gp if self.gp else self._lib.sht_inv_trans
+        return self._run(fn, spec, self.nspec_local, self.npts_grid, out, stream)
 
     def dir_trans(self, grid, out=None, stream=None):
         """Grid [nfld, npts_local] -> spectral [nfld, nspec_local] (float64)."""
-        return self._run(self._lib.sht_dir_trans, grid, self.npts_local, self.nspec_local, out, stream)
+        fn = self._lib.sht_dir_trans_gp if self.gp else self._lib.sht_dir_trans
+        return self._run(fn, grid, self.npts_grid, self.nspec_local, out, stream)
 
     def pairs_pipelined(self, host_in, host_out) -> None:
         """inv_trans + dir_trans of a stream of host batches: host_in[i] (pinned

@@ -52,6 +52,19 @@ def test_torchrun_parity(nproc, transport, recompute):
     assert "MP_OK" in res.stdout
 
 
+@pytest.mark.parametrize("nproc,gp", [(2, "2,1"), (2, "1,2"), (4, "2,2")])
+def test_torchrun_parity_gridpoint_layout(nproc, gp):
+    """2-D grid-point layout (latitude bands x longitude segments) with the ring <-> grid-point
+    transposition: every rank's grid-point slice of inv_trans, and dir_trans from grid-point
+    slices, vs the oracle."""
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    port = 29640 + 10 * nproc + (1 if gp.startswith("1") else 0)
+    res = _torchrun(nproc, "mp_check.py", ["79", "6", "639", "4"], {"MP_GP": gp, "MP_PAIRS": "2"}, port)
+    assert res.returncode == 0
+    assert "MP_OK" in res.stdout
+
+
 @pytest.mark.parametrize("transport", ["p2p", "nccl"])
 def test_dead_peer_raises_protocol_error(transport):
     if _ngpu() < 2:

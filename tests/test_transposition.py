@@ -62,3 +62,23 @@ def test_gloo_two_ranks():
         p.join(timeout=60)
     assert sorted(r for r, _ in res) == [0, 1]
     assert max(e for _, e in res) <= 1e-13
+
+
+def test_gp_bands_match_restatement(lib):
+    """libsht's latitude bands of the 2-D grid-point layout == the restatement."""
+    import numpy as np
+
+    from oracle.sht_oracle import octahedral_nloen
+    from oracle.transposition import gp_bands, gp_local
+    from paper_1908_06097_b200 import _lib
+
+    for T, nA in [(79, 1), (79, 2), (79, 3), (639, 2), (639, 4), (1279, 8)]:
+        out = np.zeros(nA + 1, dtype=np.int32)
+        _lib.check(lib.sht_gp_bands(T, 0, None, nA, out.ctypes.data_as(_lib.i32p)))
+        assert list(out) == gp_bands(octahedral_nloen(T), nA)
+    # the grid-point slices of all ranks partition the global grid
+    T, nA, nB = 31, 2, 3
+    nl = octahedral_nloen(T)
+    g = np.arange(int(nl.sum()), dtype=float)[None, :]
+    got = np.sort(np.concatenate([gp_local(g, nl, r, nA, nB)[0] for r in range(nA * nB)]))
+    assert np.array_equal(got, g[0])

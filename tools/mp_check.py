@@ -19,7 +19,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.sht_oracle import SHTransformOracle, random_grid, random_spectral  # noqa: E402
-from oracle.transposition import Layout  # noqa: E402
+from oracle.transposition import Layout, gp_local  # noqa: E402
 from paper_1908_06097_b200 import SHTransform  # noqa: E402
 
 K = int(os.environ.get("MP_PAIRS", "4"))
@@ -36,11 +36,12 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     args = [int(x) for x in sys.argv[1:]]
     recompute = bool(int(os.environ.get("SHT_RECOMPUTE", "0")))
+    gp = tuple(int(x) for x in os.environ["MP_GP"].split(",")) if os.environ.get("MP_GP") else None
     worst = 0.0
     for T, nf in zip(args[0::2], args[1::2]):
         o = SHTransformOracle(T, nfld=nf)
         lay = Layout(o, world)
-        sh = SHTransform(T, nfld=nf, group=dist.group.WORLD, recompute_legendre=recompute)
+        sh = SHTransform(T, nfld=nf, group=dist.group.WORLD, recompute_legendre=recompute, gp_layout=gp)
         assert list(sh.m_list) == list(lay.M[rank]), "m partition differs from the restatement"
         assert list(sh.ring_list) == lay.local_rings(rank), "ring partition differs"
         want = os.environ.get("SHT_TRANSPORT", "p2p")
@@ -48,7 +49,11 @@ def main():
         specs = [random_spectral(T, nf, seed=1000 * T + k) for k in range(K)]
         grids = [random_grid(T, nf, o.npts, seed=2000 * T + k) for k in range(K)]
         la = [torch.from_numpy(np.ascontiguousarray(lay.local_spec(a, rank))).cuda() for a in specs]
-        lg = [torch.from_numpy(np.ascontiguousarray(lay.local_grid(g, rank))).cuda() for g in grids]
+        if gp:  # grid side in the 2-D grid-point layout
+            local_grid = lambda x: gp_local(x, o.nloen, rank, gp[0], gp[1])  # noqa: E731
+        else:
+            local_grid = lambda x: lay.local_grid(x, rank)  # noqa: E731
+        lg = [torch.from_numpy(np.ascontiguousarray(local_grid(g))).cuda() for g in grids]
         torch.cuda.synchronize()
         gi, sd, rt = [], [], []
         for k in range(K):  # no host sync between the pairs
@@ -58,10 +63,10 @@ def main():
         sh.synchronize(timeout_ms=600000)
         e = [0.0, 0.0, 0.0]
         for k in range(K):
-            e[0] = max(e[0], rel(gi[k].cpu().numpy(), lay.local_grid(o.inv_trans(specs[k]), rank)))
+            e[0] = max(e[0], rel(gi[k].cpu().numpy(), local_grid(o.inv_trans(specs[k]))))
             e[1] = max(e[1], rel(sd[k].cpu().numpy(), lay.local_spec(o.dir_trans(grids[k]), rank)))
             e[2] = max(e[2], rel(rt[k].cpu().numpy(), lay.local_spec(specs[k], rank)))
-        print(f"rank {rank}/{world} T={T} nfld={nf} transport={sh.transport} recompute={recompute} pairs={K}: "
+        print(f"rank {rank}/{world} T={T} nfld={nf} transport={sh.transport} recompute={recompute} gp={gp} pairs={K}: "
               f"inv {e[0]:.2e} dir {e[1]:.2e} rt {e[2]:.2e}", flush=True)
         worst = max(worst, *e)
         sh.close()
