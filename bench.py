@@ -50,6 +50,8 @@ def parse():
                     help="fields in the bounded CPU sample (137 = one model level set of the 548-field batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gp-layout", default=None,
+                    help="nA,nB: grid side in the 2-D grid-point layout (adds the ring <-> grid-point transposition)")
     ap.add_argument("--recompute-legendre", action="store_true",
                     help="regenerate the P table chunk by chunk every transform (TCo1999 memory mode)")
     return ap.parse_args()
@@ -318,7 +320,9 @@ def run_ours(args):
     T, nf = args.truncation, args.nfld
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.perf_counter()
-    sh = SHTransform(T, nfld=nf, group=group, profile=True, recompute_legendre=args.recompute_legendre)
+    gp = tuple(int(x) for x in args.gp_layout.split(",")) if args.gp_layout else None
+    sh = SHTransform(T, nfld=nf, group=group, profile=True, recompute_legendre=args.recompute_legendre,
+                     gp_layout=gp)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
 
@@ -327,7 +331,7 @@ def run_ours(args):
     spec = torch.randn(nf, sh.nspec_local, dtype=torch.float64, device=dev, generator=g) / np.sqrt(2.0)
     if 0 in sh.m_list:  # Im a_n^0 = 0 (m = 0 is the first local wavenumber when present)
         spec[:, 1: 2 * (T + 1): 2] = 0.0
-    grid = torch.empty(nf, sh.npts_local, dtype=torch.float64, device=dev)
+    grid = torch.empty(nf, sh.npts_grid, dtype=torch.float64, device=dev)
     spec2 = torch.empty_like(spec)
 
     def pair():
@@ -452,6 +456,7 @@ def run_ours(args):
             "config": config_of(args),
             "layout": {"parallelism": f"m/ring-pair sharded x{world}, transposition: {transport}",
                        "transport_env": os.environ.get("SHT_TRANSPORT", "p2p (default)"),
+                       "gp_layout": args.gp_layout or "ring pairs (no grid-point transposition)",
                        "legendre": "recomputed per transform" if args.recompute_legendre else "stored table",
                        "l2": (f"no flush: inputs larger than L2 (spectral {spec.numel() * 8 / 1e9:.2f} GB, grid "
                               f"{grid.numel() * 8 / 1e9:.2f} GB per rank vs 126 MB L2)")},

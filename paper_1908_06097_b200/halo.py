@@ -63,12 +63,15 @@ def partition_block(n: int, nranks: int):
 def derive_ghosts(indptr: np.ndarray, indices: np.ndarray, owner: np.ndarray, owned: np.ndarray, rank: int):
     """Remote neighbours of this rank's owned elements as (global, owner), sorted by
     (owner, global) -- the ghost-slot order of partition.py:46-62."""
-    seen = set()
-    for g in owned:
-        for nb in indices[indptr[g]: indptr[g + 1]]:
-            if owner[nb] != rank:
-                seen.add(int(nb))
-    return sorted(((g, int(owner[g])) for g in seen), key=lambda t: (t[1], t[0]))
+    owned = np.asarray(owned, dtype=np.int64)
+    if len(owned) == 0:
+        return []
+    starts, lens = indptr[owned], indptr[owned + 1] - indptr[owned]
+    first = np.concatenate([[0], np.cumsum(lens)[:-1]])              # CSR rows of the owned elements
+    nb = indices[np.repeat(starts - first, lens) + np.arange(int(lens.sum()))]
+    remote = np.unique(nb[owner[nb] != rank])
+    order = np.lexsort((remote, owner[remote]))
+    return [(int(g), int(owner[g])) for g in remote[order]]
 
 
 @dataclass
@@ -124,18 +127,20 @@ def stencil_groups(indptr: np.ndarray, indices: np.ndarray, owned: np.ndarray, g
     """Degree groups of the neighbourhood mean (engine._stencil_ws, engine.py:237-271):
     [(degree, members (owned locals, ascending), neighbours [count, degree] as local
     indices in ascending global order per row)], degrees ascending."""
-    local_of = {int(g): i for i, g in enumerate(owned)}
-    base = len(owned)
-    for slot, (gid, _own) in enumerate(ghosts):
-        local_of[int(gid)] = base + slot
-    by_degree: dict[int, tuple[list[int], list[list[int]]]] = {}
-    for loc, g in enumerate(owned):
-        nbrs = indices[indptr[g]: indptr[g + 1]]
-        mem, rows = by_degree.setdefault(len(nbrs), ([], []))
-        mem.append(loc)
-        rows.append([local_of[int(nb)] for nb in nbrs])
-    return [(d, np.asarray(mem, dtype=np.int64), np.asarray(rows, dtype=np.int64).reshape(len(mem), d))
-            for d, (mem, rows) in sorted(by_degree.items())]
+    owned = np.asarray(owned, dtype=np.int64)
+    gg = np.asarray([g for g, _ in ghosts], dtype=np.int64)
+    keys = np.concatenate([owned, gg])
+    locs = np.arange(len(keys), dtype=np.int64)
+    srt = np.argsort(keys, kind="stable")
+    keys_s, locs_s = keys[srt], locs[srt]
+    deg = indptr[owned + 1] - indptr[owned]
+    out = []
+    for d in np.unique(deg):
+        mem = np.flatnonzero(deg == d).astype(np.int64)
+        rows = indices[indptr[owned[mem]][:, None] + np.arange(d)[None, :]]
+        pos = np.searchsorted(keys_s, rows)
+        out.append((int(d), mem, locs_s[pos].reshape(len(mem), int(d))))
+    return out
 
 
 class HaloEngine:
