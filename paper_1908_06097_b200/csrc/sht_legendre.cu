@@ -64,15 +64,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Warp-specialised pipeline: warps 0..7 consume (DMMA), warp 8 produces (bulk
-// copies).  kStages shared-memory stages, each with a "full" barrier (the
+// Warp-specialised pipeline: warps 0..7 consume (DMMA), warps 8.. produce (bulk
+// copies; 4 warps in leg_inv, 1 in leg_dir).  kStages shared-memory stages, each with a "full" barrier (the
 // producer's expect_tx arrival + the copies' transaction bytes) and an
 // "empty" barrier (one arrival per consumer warp), so no CTA-wide barrier sits
 // in the K loop and the copy issue is off the DMMA warps' path.  CTAs walk the
 // wavenumber-major tile list with a static stride (tile = blockIdx.x + k *
 // gridDim.x): the list starts with the largest K, so the interleave balances.
 constexpr int kConsumers = 8;
-constexpr int kLegThreads = 32 * (kConsumers + 1);
+constexpr int kInvProducers = 4;  // leg_inv: 4 producer warps share a stage's row copies
+constexpr int kInvThreads = 32 * (kConsumers + kInvProducers);
+constexpr int kDirThreads = 32 * (kConsumers + 1);
 constexpr int kMaxStages = 4;
 
 struct Pipe {
@@ -92,10 +94,11 @@ __device__ __forceinline__ void pipe_init(Pipe& pp) {
 }
 
 // ------------------------------------------------------------------ leg_inv
-// 2 stages of 64 wavenumbers: the 128 row copies of a stage are what the
-// TMA unit can issue under one stage's DMMA work (at 32 per stage it cannot)
-constexpr int kInvStages = 2;
-constexpr int kInvKcP = 64;                    // k-chunk (wavenumbers n) per stage
+// 4 stages of 32 wavenumbers, the 128 row copies of a stage issued by 4
+// producer warps (one warp could not issue them under a stage's DMMA work;
+// 1 warp x 2 stages of 64: 8.63 ms, 4 warps x 4 x 32: 8.32 ms at TCo639)
+constexpr int kInvStages = 4;
+constexpr int kInvKcP = 32;                    // k-chunk (wavenumbers n) per stage
 constexpr int kInvPStr = kInvKcP + 8;          // 72 doubles: P rows (== 8 mod 16 -> no LDS.128 conflicts)
 constexpr int kInvSStr = 2 * kInvKcP + 2;      // 130 doubles: field rows of the spectral tile (== 2 mod 16)
 constexpr int kInvPDbl = kInvRings * kInvPStr;
@@ -128,7 +131,7 @@ __device__ __forceinline__ InvTile inv_tile(const LegParams& p, const double* sp
   return c;
 }
 
-__global__ void __launch_bounds__(kLegThreads, 1)
+__global__ void __launch_bounds__(kInvThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) Pipe pp;
@@ -136,12 +139,13 @@ __global__ void __launch_bounds__(kLegThreads, 1)
 
   // stale operand slots must hold finite values (they meet zero P padding or
   // feed discarded accumulator rows)
-  for (int i = tid; i < kInvStages * kInvStageDbl; i += kLegThreads) sm[i] = 0.0;
+  for (int i = tid; i < kInvStages * kInvStageDbl; i += kInvThreads) sm[i] = 0.0;
   pipe_init<kInvStages>(pp);
   fence_async_smem();
   __syncthreads();
 
-  if (warp == kConsumers) {  // ---- producer: one bulk copy per P row / field row and k-chunk
+  if (warp >= kConsumers) {  // ---- producers: one bulk copy per P row / field row and k-chunk
+    const int pw = warp - kConsumers;
     int st = 0;
     unsigned ph = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
@@ -151,9 +155,9 @@ __global__ void __launch_bounds__(kLegThreads, 1)
         double* Ps = sm + st * kInvStageDbl;
         double* Ss = Ps + kInvPDbl;
         const int kcount = min(kInvKcP, c.K - kc * kInvKcP);
-        if (lane == 0) mbar_expect_tx(&pp.full[st], (unsigned)(c.nrows * kInvKcP * 8 + c.nf * kcount * 16));
+        if (pw == 0 && lane == 0) mbar_expect_tx(&pp.full[st], (unsigned)(c.nrows * kInvKcP * 8 + c.nf * kcount * 16));
         __syncwarp();
-        for (int j = lane; j < c.nrows + c.nf; j += 32) {
+        for (int j = pw * 32 + lane; j < c.nrows + c.nf; j += 32 * kInvProducers) {
           if (j < c.nrows)
             bulk_g2s(Ps + j * kInvPStr, c.P + (int64_t)j * c.kp + kc * kInvKcP, kInvKcP * 8, &pp.full[st]);
           else {
@@ -296,14 +300,14 @@ __device__ __forceinline__ DirTile dir_tile(const LegParams& p, int t) {
   return c;
 }
 
-__global__ void __launch_bounds__(kLegThreads, 1)
+__global__ void __launch_bounds__(kDirThreads, 1)
     leg_dir_kernel(const LegParams p, const double* __restrict__ four, double* __restrict__ spec) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) Pipe pp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t rowd = (int64_t)p.nfld * 4;
 
-  for (int i = tid; i < kDirStages * kDirStageDbl; i += kLegThreads) sm[i] = 0.0;
+  for (int i = tid; i < kDirStages * kDirStageDbl; i += kDirThreads) sm[i] = 0.0;
   pipe_init<kDirStages>(pp);
   fence_async_smem();
   __syncthreads();
@@ -548,7 +552,7 @@ void launch_leg_inv(const LegParams& p, const double* spec, double* four, int gr
     cudaFuncSetAttribute(leg_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
     if (dev < 64) done |= 1ull << dev;
   }
-  leg_inv_kernel<<<grid, kLegThreads, leg_inv_smem(), s>>>(p, spec, four);
+  leg_inv_kernel<<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
 }
 
 void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s) {
@@ -560,7 +564,7 @@ void launch_leg_dir(const LegParams& p, const double* four, double* spec, int gr
     cudaFuncSetAttribute(leg_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_dir_smem());
     if (dev < 64) done |= 1ull << dev;
   }
-  leg_dir_kernel<<<grid, kLegThreads, leg_dir_smem(), s>>>(p, four, spec);
+  leg_dir_kernel<<<grid, kDirThreads, leg_dir_smem(), s>>>(p, four, spec);
 }
 
 void leg_preload() {  // see fft_preload
