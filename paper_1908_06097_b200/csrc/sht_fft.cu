@@ -75,12 +75,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int V>
-struct FftCfg {
-  static constexpr int kThreads = 256;
+struct FftCfg {  // 1: 256 threads, 2 CTAs / SM; 3: rings past 100 KB, 512 threads, 1 CTA / SM
+  static constexpr int kThreads = V == 3 ? 512 : 256;
   static constexpr int kMinBlocks = V == 1 ? 2 : 1;
   template <int R>
   static constexpr bool has() {
-    return V == 1 ? (R <= 16) : true;
+    return V == 2 ? true : (R <= 16);
   }
 };
 
@@ -344,21 +344,27 @@ __device__ __forceinline__ void ring_dft(double2* buf, double2* W, int L, int ns
   }
 }
 
-// Chirp w_k = exp(-i pi k^2 / N) along a thread's walk k = k0, k0 + 256, ...
-// (k0 < 256): w_{k+256} = w_k g_k, g_{k+256} = g_k h, with g_k0 and h from the
-// arena right after the chirp table (fft_build_ring).  Two complex
-// multiplies replace an L2 load per point; ~N/256 steps keep the drift
-// at a few ulp.
+// Chirp w_k = exp(-i pi k^2 / N) along a thread's walk k = k0, k0 + NT, ...
+// (k0 < NT, NT = 256 or 512): w_{k+256} = w_k g_k, g_{k+256} = g_k h, with
+// g_t (t < 256) and h from the arena right after the chirp table
+// (fft_build_ring).  Two complex multiplies per 256 replace an L2 load per
+// point; ~N/256 steps keep the drift at a few ulp.
 struct ChirpWalk {
   double2 c, g, h;
   __device__ __forceinline__ ChirpWalk(const double2* __restrict__ chirp, int N, int k0) {
     c = k0 < N ? __ldg(chirp + k0) : make_double2(1.0, 0.0);
-    g = __ldg(chirp + N + k0);
+    g = __ldg(chirp + N + (k0 & 255));
     h = __ldg(chirp + N + 256);
+    if (k0 >= 256) g = cmul(g, h);
   }
+  template <int NT>
   __device__ __forceinline__ void step() {
-    c = cmul(c, g);
-    g = cmul(g, h);
+    static_assert(NT == 256 || NT == 512, "ChirpWalk strides by 256 or 512");
+#pragma unroll
+    for (int i = 0; i < NT / 256; ++i) {
+      c = cmul(c, g);
+      g = cmul(g, h);
+    }
   }
 };
 
@@ -421,7 +427,6 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     // grid -> smem (north -> .x, south -> .y), zero tail; Bluestein rings
     // apply the chirp on the way (register loads), the others use cp.async
     if (blue && nseq == 1) {  // one field: thread-strided k with the chirp walked in registers
-      static_assert(NT == 256, "ChirpWalk strides by 256");
       constexpr int U = 4;
       const double* src = grid + (int64_t)fb * p.grid_ld;
       ChirpWalk cw(chirp, N, threadIdx.x);
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
           const int k = k0 + u * NT;
           if (k < N) {
             buf[px(k)] = cmul(make_double2(xn[u], xs[u]), cw.c);
-            cw.step();
+            cw.step<NT>();
           } else if (k < L) {
             buf[px(k)] = make_double2(0.0, 0.0);
           }
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       for (int m = threadIdx.x; m <= M; m += NT) {
         const double2 zm = cmul(cw.c, conjc(buf[px(m)]));
         const double2 zn = m == 0 ? zm : cmul(make_double2(sg * cw.c.x, sg * cw.c.y), conjc(buf[px(N - m + rg.shift)]));
-        cw.step();
+        cw.step<NT>();
         const double2 fn = make_double2((zm.x + zn.x) * scale, (zm.y - zn.y) * scale);  // F_N
         const double2 fs = make_double2((zm.y + zn.y) * scale, (zn.x - zm.x) * scale);  // F_S
         st_slot(p.rows_out[rg.yrow_off + m] + (int64_t)fb * 4, w * (fn.x + fs.x), w * (fn.y + fs.y),
@@ -564,10 +569,9 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
     // Fourier rows -> conj(Z) at k = m and k = N - m, Z = F_N + i F_S
     // (one thread per (m, field): a row's 32-byte field slots are read once)
     if (blue && nseq == 1) {  // chirp walked along m; w_{N-m} = (-1)^N w_m
-      static_assert(NT == 256, "ChirpWalk strides by 256");
       const double sg = (N & 1) ? -1.0 : 1.0;
       ChirpWalk cw(chirp, N, threadIdx.x);
-      constexpr int U = 3;  // all of a thread's row loads in flight at once (M + 1 <= 768 in one round)
+      constexpr int U = 3;  // all of a thread's row loads in flight at once (M + 1 <= 3 NT in one round)
       for (int m0 = threadIdx.x; m0 <= M; m0 += U * NT) {
         double2 S[U], A[U];
 #pragma unroll
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
           if (m)
             buf[px(N - m + rg.shift)] =
                 cmul(make_double2(fn.x + fs.y, fn.y - fs.x), make_double2(sg * cw.c.x, sg * cw.c.y));
-          cw.step();
+          cw.step<NT>();
         }
       }
     } else
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
       double* g = grid + (int64_t)fb * p.grid_ld;
       for (int k = threadIdx.x; k < N; k += NT) {
         const double2 r = cmul(cw.c, conjc(buf[px(k ? k + rg.shift : 0)]));
-        cw.step();
+        cw.step<NT>();
         if (p.debug & 4) continue;
         __stcs(g + rg.goff_n + k, r.x);
         __stcs(g + rg.goff_s + k, -r.y);
@@ -683,12 +687,15 @@ void fft_preload() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, fft_g2f_kernel<1>);
   cudaFuncGetAttributes(&a, fft_f2g_kernel<1>);
+  cudaFuncGetAttributes(&a, fft_g2f_kernel<3>);
+  cudaFuncGetAttributes(&a, fft_f2g_kernel<3>);
 }
 
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s) {
   if (nw <= 0) return;
-  if (variant == 1 || variant == 3) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
+  if (variant == 1) launch_one<1>(g2f, p, w0, nw, in, out, smem, s);
+  if (variant == 3) launch_one<3>(g2f, p, w0, nw, in, out, smem, s);
 }
 
 // ------------------------------------------------------------------ host-side planning
