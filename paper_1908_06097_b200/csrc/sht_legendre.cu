@@ -189,22 +189,28 @@ __global__ void __launch_bounds__(kInvThreads, 1)
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[g][h][q][0] = acc[g][h][q][1] = 0.0;
-    const bool active = (c.r0 + wr * 32 < p.nh) && (c.f0 + wf * 16 < p.nfld);
+    // the tile's rings split evenly (in 8-ring groups) between the two ring
+    // warps, so a ragged last tile costs ceil(rows / 16) groups, not min(4, ceil(rows / 8))
+    const int rows = min(kInvRings, p.nh - c.r0);
+    const int split = min(kInvRings / 2, ((rows + 1) / 2 + 7) & ~7);
+    const int roff = wr ? split : 0;
+    const int nrow = wr ? rows - min(split, rows) : min(split, rows);
+    const bool active = nrow > 0 && (c.f0 + wf * 16 < p.nfld);
     // warp-uniform trims of the ragged edges: 8-ring groups, 8-field groups, 8-n sub-steps
-    const int gmax = min(4, max(0, (p.nh - c.r0 - wr * 32 + 7) / 8));
+    const int gmax = min(4, (nrow + 7) / 8);
     const int hmax = min(2, max(0, (p.nfld - c.f0 - wf * 16 + 7) / 8));
     // the epilogue's destination rows, fetched now so their latency hides under the K loop
     double* dst_row[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      const int ring = c.r0 + wr * 32 + g * 8 + (lane >> 2);
-      dst_row[g] = (active && ring < p.nh) ? p.ring_out[ring] : nullptr;
+      const int ring = c.r0 + roff + g * 8 + (lane >> 2);
+      dst_row[g] = (active && g < gmax && ring < p.nh) ? p.ring_out[ring] : nullptr;
     }
 
     for (int kc = 0; kc < c.nk; ++kc) {
       mbar_wait(&pp.full[st], ph);
       if (active) {
-        const double* Ps = sm + st * kInvStageDbl + (wr * 32 + lr) * kInvPStr + 2 * lc;
+        const double* Ps = sm + st * kInvStageDbl + (roff + lr) * kInvPStr + 2 * lc;
         const double* Ss = sm + st * kInvStageDbl + kInvPDbl + (wf * 16 + lr) * kInvSStr + 4 * lc;
         const int smax = min(kInvKcP / 8, (c.K - kc * kInvKcP + 7) / 8);
 #pragma unroll
@@ -246,8 +252,8 @@ __global__ void __launch_bounds__(kInvThreads, 1)
       const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const int ring = c.r0 + wr * 32 + g * 8 + lr;
-        if (ring < p.nh) {
+        const int ring = c.r0 + roff + g * 8 + lr;
+        if (g < gmax && ring < p.nh) {
           double* dst = dst_row[g] + (int64_t)c.lm * rowd;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
