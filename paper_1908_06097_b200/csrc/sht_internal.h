@@ -52,7 +52,7 @@ struct LegTile {  // one output tile of a Legendre GEMM
   int32_t lm;     // local wavenumber index
   int32_t r0;     // leg_inv: first northern ring; leg_dir: first n-m offset
   int32_t f0;     // first field
-  int32_t pad;
+  int32_t pad;    // leg_inv with LegParams::stage: 1 if a ring of the tile is owned by a peer
 };
 
 struct LegParams {
@@ -66,6 +66,8 @@ struct LegParams {
   int64_t spec_ld;           // doubles per local spectral field
   const int32_t* xbase;      // [nh] Fourier row of (ring i, lm = 0) in the m-side buffer (leg_dir)
   double* const* ring_out;   // [nh] leg_inv: row of (ring i, lm = 0) in the ring owner's receive buffer
+  double* stage;             // leg_inv: [grid][2][64 rings][64 fields][4] staging slots of the
+                             // pusher epilogue (p2p, P > 1), or nullptr
   const double* ptab;        // P table
   const LegTile* tiles;
   int ntiles;

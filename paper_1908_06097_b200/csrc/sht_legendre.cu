@@ -82,6 +82,25 @@ struct Pipe {
   uint64_t empty[kMaxStages];
 };
 
+// leg_inv's staged epilogue (p2p transport, tiles with rings owned by a peer):
+// the consumers park the finished tile in a per-CTA slot of local HBM and
+// move on; the pusher warp (the last producer warp) streams it to the ring
+// owners over NVLink while the next tile's GEMM runs.  "staged" completes when
+// the 8 consumer warps have written a slot, "freed" when the pusher has read it.
+constexpr int kStageSlots = 2;
+constexpr int64_t kStageDbl = (int64_t)kInvRings * kLegFields * 4;
+struct StagePipe {
+  uint64_t staged[kStageSlots];
+  uint64_t freed[kStageSlots];
+};
+
+__device__ __forceinline__ void st_stage(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_stage(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
+}
+
 template <int kStages>
 __device__ __forceinline__ void pipe_init(Pipe& pp) {
   if (threadIdx.x == 0) {
@@ -135,17 +154,65 @@ __global__ void __launch_bounds__(kInvThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) Pipe pp;
+  __shared__ __align__(8) StagePipe sp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool staging = p.stage != nullptr;
 
   // stale operand slots must hold finite values (they meet zero P padding or
   // feed discarded accumulator rows)
   for (int i = tid; i < kInvStages * kInvStageDbl; i += kInvThreads) sm[i] = 0.0;
   pipe_init<kInvStages>(pp);
+  if (tid == 0) {
+    for (int s = 0; s < kStageSlots; ++s) {
+      mbar_init(&sp.staged[s], kConsumers);
+      mbar_init(&sp.freed[s], 1);
+    }
+    fence_mbar_init();
+  }
   fence_async_smem();
   __syncthreads();
 
+  if (staging && warp == kConsumers + kInvProducers - 1) {  // ---- pusher
+    const int64_t rowd = (int64_t)p.nfld * 4;
+    int k = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      if (!p.tiles[t].pad) continue;
+      const InvTile c = inv_tile(p, spec, t);
+      const int slot = k & 1;
+      mbar_wait(&sp.staged[slot], (k >> 1) & 1);
+      ++k;
+      const double* src = p.stage + ((int64_t)blockIdx.x * kStageSlots + slot) * kStageDbl;
+      for (int r0 = 0; r0 < c.nrows; r0 += 4) {  // 8 slot loads in flight per lane
+        double v[4][2][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int r = r0 + a, f = lane + 32 * b;
+            if (r < c.nrows && f < c.nf)
+              ld_stage(src + ((int64_t)r * kLegFields + f) * 4, v[a][b][0], v[a][b][1], v[a][b][2], v[a][b][3]);
+          }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int r = r0 + a;
+          if (r >= c.nrows) break;
+          double* dst = p.ring_out[c.r0 + r] + (int64_t)c.lm * rowd + (int64_t)c.f0 * 4;
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int f = lane + 32 * b;
+            if (f < c.nf) st_slot(dst + (int64_t)f * 4, v[a][b][0], v[a][b][1], v[a][b][2], v[a][b][3]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sp.freed[slot]);  // every load of the slot has returned
+    }
+    return;
+  }
+
   if (warp >= kConsumers) {  // ---- producers: one bulk copy per P row / field row and k-chunk
     const int pw = warp - kConsumers;
+    const int nprod = staging ? kInvProducers - 1 : kInvProducers;
     int st = 0;
     unsigned ph = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
@@ -157,7 +224,7 @@ __global__ void __launch_bounds__(kInvThreads, 1)
         const int kcount = min(kInvKcP, c.K - kc * kInvKcP);
         if (pw == 0 && lane == 0) mbar_expect_tx(&pp.full[st], (unsigned)(c.nrows * kInvKcP * 8 + c.nf * kcount * 16));
         __syncwarp();
-        for (int j = pw * 32 + lane; j < c.nrows + c.nf; j += 32 * kInvProducers) {
+        for (int j = pw * 32 + lane; j < c.nrows + c.nf; j += 32 * nprod) {
           if (j < c.nrows)
             bulk_g2s(Ps + j * kInvPStr, c.P + (int64_t)j * c.kp + kc * kInvKcP, kInvKcP * 8, &pp.full[st]);
           else {
@@ -180,8 +247,10 @@ __global__ void __launch_bounds__(kInvThreads, 1)
   const int lr = lane >> 2, lc = lane & 3;
   int st = 0;
   unsigned ph = 0;
+  int ks = 0;  // staged tiles so far
   for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     const InvTile c = inv_tile(p, spec, t);
+    const bool staged = staging && p.tiles[t].pad;
     double acc[4][2][4][2];
 #pragma unroll
     for (int g = 0; g < 4; ++g)
@@ -204,7 +273,7 @@ __global__ void __launch_bounds__(kInvThreads, 1)
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const int ring = c.r0 + roff + g * 8 + (lane >> 2);
-      dst_row[g] = (active && g < gmax && ring < p.nh) ? p.ring_out[ring] : nullptr;
+      dst_row[g] = (active && !staged && g < gmax && ring < p.nh) ? p.ring_out[ring] : nullptr;
     }
 
     for (int kc = 0; kc < c.nk; ++kc) {
@@ -246,9 +315,35 @@ __global__ void __launch_bounds__(kInvThreads, 1)
       }
     }
     // epilogue: each (ring, field) slot as one 256-bit store straight into the
-    // ring owner's receive buffer (local, or a peer GPU over NVLink); the
-    // producer keeps filling the next tile's stages meanwhile
-    if (active && !(p.debug & 4)) {
+    // ring owner's receive buffer (local, or a peer GPU over NVLink), or -- a
+    // staged tile -- into this CTA's staging slot for the pusher; the producers
+    // keep filling the next tile's stages meanwhile
+    if (staged) {
+      const int slot = ks & 1;
+      mbar_wait(&sp.freed[slot], ((ks >> 1) & 1) ^ 1);  // the pusher has drained this slot's last tile
+      ++ks;
+      if (active && !(p.debug & 4)) {
+        double* sdst = p.stage + ((int64_t)blockIdx.x * kStageSlots + slot) * kStageDbl;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int rl = roff + g * 8 + lr;
+          if (g < gmax && c.r0 + rl < p.nh) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int fl = wf * 16 + h * 8 + 2 * lc + e;
+                if (c.f0 + fl < p.nfld)
+                  st_stage(sdst + ((int64_t)rl * kLegFields + fl) * 4, acc[g][h][0][e], acc[g][h][1][e],
+                           acc[g][h][2][e], acc[g][h][3][e]);
+              }
+          }
+        }
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sp.staged[slot]);
+    } else if (active && !(p.debug & 4)) {
       const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {

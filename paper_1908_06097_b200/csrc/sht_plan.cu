@@ -250,6 +250,8 @@ struct sht_plan {
   std::vector<int64_t> orow;                    //   and the row in the owner's X
   std::vector<int64_t> yoff_at_owner;           // per ring owner d: row offset of block r in d's Y
   double** d_ring_out = nullptr;                // [nh] leg_inv destination row of (ring, lm = 0)
+  double* d_stage = nullptr;                    // leg_inv pusher-epilogue staging slots (p2p, P > 1)
+  std::vector<sht::LegTile> h_tiles_inv;        // host copy of the leg_inv tile list
   double** d_rows_out = nullptr;                // fft_g2f destination row per (local ring, m)
   const double** d_rows_in = nullptr;           // fft_f2g source row per (local ring, m)
   // 2-D grid-point layout (sht_plan_set_gp_layout): the TRGTOL-style transposition
@@ -285,7 +287,7 @@ static void free_plan(sht_plan* p) {
                   p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->flagw, p->d_peer_flags,
                   p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in, p->d_gp_send_idx, p->d_gp_recv_idx,
-                  p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1};
+                  p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1, p->d_stage};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_events) {
@@ -627,6 +629,23 @@ static int build_transport(sht_plan* p) {
     rows_out[k] = p->p2p ? p->peer_x[p->orow_owner[k]] + p->orow[k] * rowd : p->Y + p->yrow[k] * rowd;
   }
   if (int rc = upload(&p->d_ring_out, ring_out)) return rc;
+  // p2p: leg_inv tiles with a ring owned by a peer take the staged (pusher)
+  // epilogue, so the NVLink stores leave the DMMA warps' path (SHT_LEG_STAGE=0: direct stores)
+  const char* stg = getenv("SHT_LEG_STAGE");
+  if (p->p2p && p->nranks > 1 && !(stg && std::string(stg) == "0") && p->ntiles_inv > 0) {
+    std::vector<LegTile> ti = p->h_tiles_inv;
+    bool any = false;
+    for (auto& t : ti) {
+      t.pad = 0;
+      for (int i = t.r0; i < std::min(nh, t.r0 + kInvRings); ++i)
+        if (p->ring_owner[i] != p->rank) t.pad = 1;
+      any = any || t.pad;
+    }
+    if (any) {
+      SHT_CUDA_TRY(cudaMemcpy(p->d_tiles_inv, ti.data(), ti.size() * sizeof(LegTile), cudaMemcpyHostToDevice));
+      SHT_CUDA_TRY(cudaMalloc((void**)&p->d_stage, (size_t)p->nsm * 2 * kInvRings * kLegFields * 4 * sizeof(double)));
+    }
+  }
   if (int rc = upload(&p->d_rows_out, rows_out)) return rc;
   if (int rc = upload(&p->d_rows_in, rows_in)) return rc;
   return SHT_OK;
@@ -741,6 +760,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   }
   p->ntiles_inv = (int)ti.size();
   p->ntiles_dir = (int)td.size();
+  p->h_tiles_inv = ti;
 
   // grid layout + FFT plans
   const int nlr = (int)p->my_rings.size();
@@ -974,6 +994,7 @@ static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles,
   lp.spec_ld = p->spec_ld;
   lp.xbase = p->d_xbase;
   lp.ring_out = p->d_ring_out;
+  lp.stage = p->d_stage;
   lp.ptab = p->d_ptab;
   lp.tiles = tiles;
   lp.ntiles = ntiles;
