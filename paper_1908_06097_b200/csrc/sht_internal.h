@@ -46,6 +46,7 @@ constexpr int kInvRings = 64;
 constexpr int kInvKc = 64;
 constexpr int kDirN = 128;
 constexpr int kDirKc = 32;
+constexpr int kStageSlots = 2;  // leg_inv pusher epilogue: staging slots per CTA
 constexpr int kPtabPad = 64;  // P-table rows are padded (with zeros) to a multiple of this
 
 struct LegTile {  // one output tile of a Legendre GEMM

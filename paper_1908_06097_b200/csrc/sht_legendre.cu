@@ -87,7 +87,6 @@ struct Pipe {
 // move on; the pusher warp (the last producer warp) streams it to the ring
 // owners over NVLink while the next tile's GEMM runs.  "staged" completes when
 // the 8 consumer warps have written a slot, "freed" when the pusher has read it.
-constexpr int kStageSlots = 2;
 constexpr int64_t kStageDbl = (int64_t)kInvRings * kLegFields * 4;
 struct StagePipe {
   uint64_t staged[kStageSlots];

@@ -643,7 +643,7 @@ static int build_transport(sht_plan* p) {
     }
     if (any) {
       SHT_CUDA_TRY(cudaMemcpy(p->d_tiles_inv, ti.data(), ti.size() * sizeof(LegTile), cudaMemcpyHostToDevice));
-      SHT_CUDA_TRY(cudaMalloc((void**)&p->d_stage, (size_t)p->nsm * 2 * kInvRings * kLegFields * 4 * sizeof(double)));
+      SHT_CUDA_TRY(cudaMalloc((void**)&p->d_stage, (size_t)p->nsm * kStageSlots * kInvRings * kLegFields * 4 * sizeof(double)));
     }
   }
   if (int rc = upload(&p->d_rows_out, rows_out)) return rc;
