@@ -19,8 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsht.so"
 OBJ = ROOT / "build" / "obj"
-SOURCES = ["sht_plan.cu", "sht_legendre.cu", "sht_fft.cu", "sht_halo.cu", "sht_gp.cu"]
-HEADERS = ["sht_internal.h", "fft_codelets.cuh"]
+SOURCES = ["sht_plan.cu", "sht_legendre.cu", "sht_fft.cu", "sht_fft_blk.cu", "sht_halo.cu", "sht_gp.cu"]
+HEADERS = ["sht_internal.h", "fft_codelets.cuh", "fft_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -47,6 +47,14 @@ constexpr int kInvKc = 64;
 constexpr int kDirN = 128;
 constexpr int kDirKc = 32;
 constexpr int kStageSlots = 2;  // leg_inv pusher epilogue: staging slots per CTA
+// Fourier-row buffers (X, Y): field slot f (S.re, S.im, A.re, A.im) of row
+// `row` sits at base + (f >> fsh) * bs + row * row_ld + (f & fmask) * 4.
+// Classic layout (P = 1, NCCL): one row holds every field (row_ld = 4 nfld,
+// fsh = 30).  Field-blocked layout (p2p, P > 1): [64-field block][row][64][4]
+// (row_ld = kRowDbl, fsh = 6, bs = rows x kRowDbl): a ring's rows are 2 KB
+// apart in each block, which keeps the remote footprint of the scattered
+// NVLink row stores small (profiles/r02_transport_cliff.md).
+constexpr int kRowDbl = kLegFields * 4;
 constexpr int kPtabPad = 64;  // P-table rows are padded (with zeros) to a multiple of this
 
 struct LegTile {  // one output tile of a Legendre GEMM
@@ -66,7 +74,11 @@ struct LegParams {
   const int64_t* lm_soff;    // [nlm] complex offset of (m, n = m) in the local spectral field
   int64_t spec_ld;           // doubles per local spectral field
   const int32_t* xbase;      // [nh] Fourier row of (ring i, lm = 0) in the m-side buffer (leg_dir)
-  double* const* ring_out;   // [nh] leg_inv: row of (ring i, lm = 0) in the ring owner's receive buffer
+  double* const* ring_out;   // [nh] leg_inv: row of (ring i, lm = 0), field block 0, in the ring owner's receive buffer
+  const int64_t* ring_bs;    // [nh] field-block stride (doubles) of that buffer
+  int64_t xbs;               // leg_dir: field-block stride of X
+  int64_t row_ld;            // doubles between consecutive rows (of one field block)
+  int fsh, fmask;            // field f -> block f >> fsh, slot f & fmask
   double* stage;             // leg_inv: [grid][2][64 rings][64 fields][4] staging slots of the
                              // pusher epilogue (p2p, P > 1), or nullptr
   const double* ptab;        // P table
@@ -152,16 +164,21 @@ struct FftParams {
   const FftStep* steps;
   const FftWork* work;
   const double2* tw;         // twiddle / chirp arena
-  double* const* rows_out;   // g2f: Fourier row (field 0) of (ring, m) in the m-owner's receive buffer
-  const double* const* rows_in;  // f2g: Fourier row (field 0) of (ring, m) in this rank's receive buffer
+  double* const* rows_out;   // g2f: Fourier row (field block 0) of (ring, m) in the m-owner's receive buffer
+  const int64_t* rows_out_bs;    // its field-block stride (doubles)
+  const double* const* rows_in;  // f2g: Fourier row (field block 0) of (ring, m) in this rank's receive buffer
+  int64_t in_bs;                 // field-block stride of that buffer
+  int fsh, fmask;                // field f -> block f >> fsh, slot f & fmask
   int debug;                 // profiling only (SHT_FFT_DEBUG): bit 0 skips the DFT steps
 };
 
-// Ring-FFT launch classes: 1 = pencils <= 16 points, 256 threads, <= 104 KB
-// (2 CTAs/SM); 2 = pencils up to 31 points (primes 17..31), 1 CTA/SM;
-// 3 = class-1 kernel with up to 212 KB of shared memory (1 CTA/SM).
+// Ring-FFT launch classes: 1 = 256 threads, <= 100 KB of shared memory
+// (2 CTAs/SM); 3 = 512 threads, up to 212 KB (1 CTA/SM); 2 is unused.
 constexpr int kFftVariants = 4;  // index 0 unused
 void fft_preload();  // load every kernel of the file now (no lazy load inside a transform)
+void fft_preload_blk();  // the field-blocked-layout kernels (sht_fft_blk.cu)
+void launch_fft_blk(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
+                    size_t smem, cudaStream_t s);
 void launch_fft(bool g2f, int variant, const FftParams& p, int w0, int nw, const double* in, double* out,
                 size_t smem, cudaStream_t s);
 

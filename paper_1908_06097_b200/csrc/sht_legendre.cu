@@ -149,19 +149,20 @@ __device__ __forceinline__ InvTile inv_tile(const LegParams& p, const double* sp
   return c;
 }
 
+template <bool kStaged>
 __global__ void __launch_bounds__(kInvThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) Pipe pp;
   __shared__ __align__(8) StagePipe sp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool staging = p.stage != nullptr;
+  constexpr bool staging = kStaged;  // p.stage != nullptr
 
   // stale operand slots must hold finite values (they meet zero P padding or
   // feed discarded accumulator rows)
   for (int i = tid; i < kInvStages * kInvStageDbl; i += kInvThreads) sm[i] = 0.0;
   pipe_init<kInvStages>(pp);
-  if (tid == 0) {
+  if (staging && tid == 0) {
     for (int s = 0; s < kStageSlots; ++s) {
       mbar_init(&sp.staged[s], kConsumers);
       mbar_init(&sp.freed[s], 1);
@@ -172,7 +173,6 @@ __global__ void __launch_bounds__(kInvThreads, 1)
   __syncthreads();
 
   if (staging && warp == kConsumers + kInvProducers - 1) {  // ---- pusher
-    const int64_t rowd = (int64_t)p.nfld * 4;
     int k = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       if (!p.tiles[t].pad) continue;
@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kInvThreads, 1)
         for (int a = 0; a < 4; ++a) {
           const int r = r0 + a;
           if (r >= c.nrows) break;
-          double* dst = p.ring_out[c.r0 + r] + (int64_t)c.lm * rowd + (int64_t)c.f0 * 4;
+          double* dst = p.ring_out[c.r0 + r] + (c.f0 >> p.fsh) * p.ring_bs[c.r0 + r] + c.lm * p.row_ld +
+                        (c.f0 & p.fmask) * 4;
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
             const int f = lane + 32 * b;
@@ -272,7 +273,9 @@ __global__ void __launch_bounds__(kInvThreads, 1)
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const int ring = c.r0 + roff + g * 8 + (lane >> 2);
-      dst_row[g] = (active && !staged && g < gmax && ring < p.nh) ? p.ring_out[ring] : nullptr;
+      dst_row[g] = (active && !staged && g < gmax && ring < p.nh)
+                       ? p.ring_out[ring] + (c.f0 >> p.fsh) * p.ring_bs[ring] + c.lm * p.row_ld + (c.f0 & p.fmask) * 4
+                       : nullptr;
     }
 
     for (int kc = 0; kc < c.nk; ++kc) {
@@ -343,19 +346,18 @@ __global__ void __launch_bounds__(kInvThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sp.staged[slot]);
     } else if (active && !(p.debug & 4)) {
-      const int64_t rowd = (int64_t)p.nfld * 4;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const int ring = c.r0 + roff + g * 8 + lr;
         if (g < gmax && ring < p.nh) {
-          double* dst = dst_row[g] + (int64_t)c.lm * rowd;
+          double* dst = dst_row[g];
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int f = c.f0 + wf * 16 + h * 8 + 2 * lc + e;
-              if (f < p.nfld)
-                st_slot(dst + (int64_t)f * 4, acc[g][h][0][e], acc[g][h][1][e], acc[g][h][2][e], acc[g][h][3][e]);
+              const int fl = wf * 16 + h * 8 + 2 * lc + e;
+              if (c.f0 + fl < p.nfld)
+                st_slot(dst + fl * 4, acc[g][h][0][e], acc[g][h][1][e], acc[g][h][2][e], acc[g][h][3][e]);
             }
         }
       }
@@ -405,7 +407,6 @@ __global__ void __launch_bounds__(kDirThreads, 1)
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) Pipe pp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rowd = (int64_t)p.nfld * 4;
 
   for (int i = tid; i < kDirStages * kDirStageDbl; i += kDirThreads) sm[i] = 0.0;
   pipe_init<kDirStages>(pp);
@@ -434,8 +435,10 @@ __global__ void __launch_bounds__(kDirThreads, 1)
           const int rr = j >> 1;
           const int ring = kc * kDirKcR + rr;  // relative to i0
           if (j & 1)
-            bulk_g2s(Bs + rr * kDirBStr + dir_boff(rr), four + (int64_t)(p.xbase[c.i0 + ring] + c.lm) * rowd +
-                     (int64_t)c.f0 * 4, c.nf * 32, &pp.full[st]);
+            bulk_g2s(Bs + rr * kDirBStr + dir_boff(rr),
+                     four + (c.f0 >> p.fsh) * p.xbs + (p.xbase[c.i0 + ring] + c.lm) * p.row_ld + (c.f0 & p.fmask) * 4,
+                     c.nf * 32,
+                     &pp.full[st]);
           else
             bulk_g2s(Ps + rr * kDirPStr, c.P + (int64_t)ring * c.kp + c.n0, pbytes, &pp.full[st]);
         }
@@ -649,10 +652,14 @@ void launch_leg_inv(const LegParams& p, const double* spec, double* four, int gr
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 64 || !(done >> dev & 1)) {
-    cudaFuncSetAttribute(leg_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
     if (dev < 64) done |= 1ull << dev;
   }
-  leg_inv_kernel<<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
+  if (p.stage)
+    leg_inv_kernel<true><<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
+  else
+    leg_inv_kernel<false><<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
 }
 
 void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s) {
@@ -669,7 +676,8 @@ void launch_leg_dir(const LegParams& p, const double* four, double* spec, int gr
 
 void leg_preload() {  // see fft_preload
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, leg_inv_kernel);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<false>);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<true>);
   cudaFuncGetAttributes(&a, leg_dir_kernel);
   cudaFuncGetAttributes(&a, leg_poly_kernel);
   cudaFuncGetAttributes(&a, leg_diag_kernel);

@@ -194,6 +194,10 @@ struct sht_plan {
   int64_t spec_ld = 0, grid_ld = 0;
   std::vector<int64_t> xoff, xrows, yoff, yrows;  // per peer, in rows
   int64_t xtot = 0, ytot = 0;
+  std::vector<int64_t> xtot_of, ytot_of;         // every rank's X / Y row count (field-block strides)
+  int nfb = 1;                                   // 64-field blocks of the Fourier-row buffers
+  bool fblk = false;                             // field-blocked row layout (p2p, P > 1), else classic
+  int64_t row_ld = 0;                            // doubles between consecutive rows (sht_internal.h)
   double work_leg = 0, work_fft = 0, work_a2a = 0;
 
   // device
@@ -251,6 +255,8 @@ struct sht_plan {
   std::vector<int64_t> yoff_at_owner;           // per ring owner d: row offset of block r in d's Y
   double** d_ring_out = nullptr;                // [nh] leg_inv destination row of (ring, lm = 0)
   double* d_stage = nullptr;                    // leg_inv pusher-epilogue staging slots (p2p, P > 1)
+  int64_t* d_ring_bs = nullptr;                 // [nh] field-block stride of ring_out's buffer
+  int64_t* d_rows_out_bs = nullptr;             // field-block stride of each rows_out row's buffer
   std::vector<sht::LegTile> h_tiles_inv;        // host copy of the leg_inv tile list
   double** d_rows_out = nullptr;                // fft_g2f destination row per (local ring, m)
   const double** d_rows_in = nullptr;           // fft_f2g source row per (local ring, m)
@@ -287,7 +293,8 @@ static void free_plan(sht_plan* p) {
                   p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
                   p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->flagw, p->d_peer_flags,
                   p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in, p->d_gp_send_idx, p->d_gp_recv_idx,
-                  p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1, p->d_stage};
+                  p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1, p->d_stage,
+                  p->d_ring_bs, p->d_rows_out_bs};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->have_events) {
@@ -360,7 +367,7 @@ static int build_partition(const Geometry& g, int P, std::vector<int>& m_owner, 
 
 // ------------------------------------------------------------------ transposition
 enum FlagSlot { kYArr = 0, kXArr = 1, kYFree = 2, kXFree = 3 };
-constexpr double kP2PMaxBytes = 8.0 * (1 << 30);  // largest receive buffer the p2p transport stores into
+constexpr double kP2PMaxBytes = 2.0 * (1 << 30);  // largest receive buffer for the classic row layout under p2p
 
 // Handshake of the p2p transposition, one thread per peer t: publish
 // `sig_v` in slot `sig_slot` of peer t's flag words (release, system scope:
@@ -534,25 +541,23 @@ static int close_barrier(sht_plan* p) {
 // peers or all fall back to NCCL send/recv.
 static int build_transport(sht_plan* p) {
   const int P = p->nranks, r = p->rank;
-  const size_t rowd = (size_t)p->nfld * 4;
   p->peer_x.assign(P, nullptr);
   p->peer_y.assign(P, nullptr);
   p->peer_flags.assign(P, nullptr);
   p->peer_x[r] = p->X;
   p->peer_y[r] = p->Y;
   if (P > 1) {
-    // p2p unless SHT_TRANSPORT=nccl, or (without SHT_TRANSPORT=p2p) the
-    // receive buffers the kernels would store into over NVLink are large and
-    // spread over >= 2 peers, where the scattered remote row stores fall off
-    // a translation cliff: at TCo1999 x 548 on 4 B200 (13 GB per rank) the
-    // fused fft_g2f took 120 ms against 49 ms with local stores + NCCL, while
-    // 13 GB on 2 B200 and 6.6 GB on 4 B200 showed no cliff
-    // (profiles/r02_transport_cliff.md)
+    // p2p unless SHT_TRANSPORT=nccl (or a rank cannot map its peers).  Where
+    // the receive buffers the kernels store into over NVLink are large and
+    // spread over >= 2 peers, the scattered remote row stores of the classic
+    // row layout fall off a translation cliff (TCo1999 x 548 on 4 B200, 13 GB
+    // per rank: fft_g2f 120 ms against 49 ms with local stores; 13 GB on 2
+    // B200 showed none, profiles/r02_transport_cliff.md):
+    // there the plan switches to the field-blocked row layout (fblk below).
     const char* tr = getenv("SHT_TRANSPORT");
     const double rbuf = (double)std::max(p->xtot, p->ytot) * (double)p->nfld * 32.0;
-    const bool force_p2p = tr && std::string(tr) == "p2p";
     const bool cliff = P >= 3 && rbuf > kP2PMaxBytes;
-    const bool want = !(tr && std::string(tr) == "nccl") && (force_p2p || !cliff);
+    const bool want = !(tr && std::string(tr) == "nccl");
     SHT_CUDA_TRY(cudaMalloc((void**)&p->flagw, 4 * P * sizeof(uint32_t)));
     SHT_CUDA_TRY(cudaMemset(p->flagw, 0, 4 * P * sizeof(uint32_t)));
     p->peer_flags[r] = p->flagw;
@@ -567,6 +572,7 @@ static int build_transport(sht_plan* p) {
     mine.ok[0] = want && cudaIpcGetMemHandle(&mine.h[0], p->X) == cudaSuccess &&
                  cudaIpcGetMemHandle(&mine.h[1], p->Y) == cudaSuccess &&
                  cudaIpcGetMemHandle(&mine.h[2], p->flagw) == cudaSuccess;
+    mine.ok[1] = cliff;
     cudaGetLastError();
     Rec* d = nullptr;
     SHT_CUDA_TRY(cudaMalloc((void**)&d, (P + 1) * sizeof(Rec)));
@@ -582,6 +588,7 @@ static int build_transport(sht_plan* p) {
     int rc = exchange();
     bool ok = rc == SHT_OK;
     for (int t = 0; t < P && ok; ++t) ok = all[t].ok[0] != 0;
+    for (int t = 0; t < P && rc == SHT_OK; ++t) p->fblk = p->fblk || all[t].ok[1] != 0;  // any rank past the cliff
     if (ok) {  // map every peer, then agree that everybody could
       for (int t = 0; t < P && ok; ++t) {
         if (t == r) continue;
@@ -617,18 +624,35 @@ static int build_transport(sht_plan* p) {
   }
   // row pointers: leg_inv's destination per ring, fft_g2f's per (ring, m), fft_f2g's source per (ring, m)
   const int nh = p->g.nh;
+  // row layout: field-blocked where the p2p kernels' scattered remote row
+  // stores would fall off the translation cliff (agreed above: any rank's
+  // receive buffer > 2 GiB with >= 3 ranks; TCo1279 x 548 on 4 B200, 5.4 GB,
+  // measured 73.3 ms classic vs 64.4 ms blocked on one box, 64.3 classic on
+  // another; TCo639 x 548, 0.9 GB: 11.73 classic vs ~12.0 blocked); SHT_ROW_LAYOUT=classic|blocked
+  // overrides (set it identically on every rank)
+  p->fblk = p->p2p && p->fblk;
+  if (const char* lay = getenv("SHT_ROW_LAYOUT")) p->fblk = std::string(lay) == "blocked";
+  p->row_ld = p->fblk ? kRowDbl : (int64_t)p->nfld * 4;
+  const int64_t ld = p->row_ld;
+  auto bs = [&](int64_t rows) { return p->fblk ? rows * kRowDbl : (int64_t)0; };
   std::vector<double*> ring_out(nh), rows_out(p->yrow.size());
   std::vector<const double*> rows_in(p->yrow.size());
+  std::vector<int64_t> ring_bs(nh), rows_out_bs(p->yrow.size());
   for (int i = 0; i < nh; ++i) {
     const int d = p->ring_owner[i];
-    ring_out[i] = p->p2p ? p->peer_y[d] + (p->xbase[i] - p->xoff[d] + p->yoff_at_owner[d]) * rowd
-                         : p->X + (size_t)p->xbase[i] * rowd;
+    ring_out[i] = p->p2p ? p->peer_y[d] + (p->xbase[i] - p->xoff[d] + p->yoff_at_owner[d]) * ld
+                         : p->X + (size_t)p->xbase[i] * ld;
+    ring_bs[i] = bs(p->p2p ? p->ytot_of[d] : p->xtot);
   }
   for (size_t k = 0; k < p->yrow.size(); ++k) {
-    rows_in[k] = p->Y + p->yrow[k] * rowd;
-    rows_out[k] = p->p2p ? p->peer_x[p->orow_owner[k]] + p->orow[k] * rowd : p->Y + p->yrow[k] * rowd;
+    const int t = p->orow_owner[k];
+    rows_in[k] = p->Y + p->yrow[k] * ld;
+    rows_out[k] = p->p2p ? p->peer_x[t] + p->orow[k] * ld : p->Y + p->yrow[k] * ld;
+    rows_out_bs[k] = bs(p->p2p ? p->xtot_of[t] : p->ytot);
   }
   if (int rc = upload(&p->d_ring_out, ring_out)) return rc;
+  if (int rc = upload(&p->d_ring_bs, ring_bs)) return rc;
+  if (int rc = upload(&p->d_rows_out_bs, rows_out_bs)) return rc;
   // p2p: leg_inv tiles with a ring owned by a peer take the staged (pusher)
   // epilogue, so the NVLink stores leave the DMMA warps' path (SHT_LEG_STAGE=0: direct stores)
   const char* stg = getenv("SHT_LEG_STAGE");
@@ -718,6 +742,16 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
       for (int i : Rlist[d]) xoff_at_owner[t] += cnt[t][i];
   p->xbase = xbase;
   if (p->xtot > INT32_MAX || p->ytot > INT32_MAX) return fail(SHT_ERR_CONFIG, "Fourier row count overflows int32");
+  // every rank's buffer heights: the field-block strides of the peers' X / Y (p2p)
+  p->nfb = (nfld + kLegFields - 1) / kLegFields;
+  p->xtot_of.assign(P, 0);
+  p->ytot_of.assign(P, 0);
+  for (int t = 0; t < P; ++t)
+    for (int i = 0; i < nh; ++i) p->xtot_of[t] += cnt[t][i];
+  for (int d = 0; d < P; ++d)
+    for (int s2 = 0; s2 < P; ++s2)
+      for (int i : Rlist[d]) p->ytot_of[d] += cnt[s2][i];
+  if (p->xtot_of[r] != p->xtot || p->ytot_of[r] != p->ytot) return fail(SHT_ERR_CONFIG, "row-count bookkeeping");
 
   // local spectral layout
   p->lm_soff.resize(nlm);
@@ -903,7 +937,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   if (int rc = upload(&p->d_steps, steps)) return rc;
   if (int rc = upload(&p->d_tw, arena)) return rc;
   SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
-  const size_t rowb = (size_t)nfld * 4 * sizeof(double);
+  const size_t rowb = (size_t)p->nfb * kRowDbl * sizeof(double);  // one row in every field block
   SHT_CUDA_TRY(cudaMalloc((void**)&p->X, std::max<int64_t>(p->xtot, 1) * rowb));
   if (P == 1) {
     p->Y = p->X;
@@ -995,6 +1029,11 @@ static LegParams leg_params(const sht_plan* p, const LegTile* tiles, int ntiles,
   lp.xbase = p->d_xbase;
   lp.ring_out = p->d_ring_out;
   lp.stage = p->d_stage;
+  lp.ring_bs = p->d_ring_bs;
+  lp.xbs = p->fblk ? p->xtot * kRowDbl : 0;
+  lp.row_ld = p->row_ld;
+  lp.fsh = p->fblk ? 6 : 30;
+  lp.fmask = p->fblk ? 63 : (1 << 30) - 1;
   lp.ptab = p->d_ptab;
   lp.tiles = tiles;
   lp.ntiles = ntiles;
@@ -1013,6 +1052,10 @@ static FftParams fft_params(const sht_plan* p) {
   fp.tw = p->d_tw;
   fp.rows_out = p->d_rows_out;
   fp.rows_in = p->d_rows_in;
+  fp.rows_out_bs = p->d_rows_out_bs;
+  fp.in_bs = p->fblk ? p->ytot * kRowDbl : 0;
+  fp.fsh = p->fblk ? 6 : 30;
+  fp.fmask = p->fblk ? 63 : (1 << 30) - 1;
   fp.debug = p->fft_debug;
   return fp;
 }
@@ -1023,25 +1066,31 @@ static FftParams fft_params(const sht_plan* p) {
 // device copy.  from_x: X -> Y (inverse), else Y -> X (direct).
 static int alltoall(sht_plan* p, bool from_x, cudaStream_t s) {
   const int P = p->nranks, r = p->rank;
-  const size_t rowd = (size_t)p->nfld * 4;
+  const size_t rowd = p->row_ld;
+  const int nblk = p->fblk ? p->nfb : 1;
   const double* src = from_x ? p->X : p->Y;
   double* dst = from_x ? p->Y : p->X;
+  const size_t sbs = (size_t)(from_x ? p->xtot : p->ytot) * rowd;  // field-block strides (blocked layout)
+  const size_t dbs = (size_t)(from_x ? p->ytot : p->xtot) * rowd;
   const std::vector<int64_t>& soff = from_x ? p->xoff : p->yoff;
   const std::vector<int64_t>& srows = from_x ? p->xrows : p->yrows;
   const std::vector<int64_t>& doff = from_x ? p->yoff : p->xoff;
   const std::vector<int64_t>& drows = from_x ? p->yrows : p->xrows;
-  if (srows[r] > 0)
-    SHT_CUDA_TRY(cudaMemcpyAsync(dst + doff[r] * rowd, src + soff[r] * rowd, srows[r] * rowd * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, s));
+  if (srows[r] > 0)  // the self block of every field block
+    SHT_CUDA_TRY(cudaMemcpy2DAsync(dst + doff[r] * rowd, dbs * sizeof(double), src + soff[r] * rowd,
+                                   sbs * sizeof(double), srows[r] * rowd * sizeof(double), nblk,
+                                   cudaMemcpyDeviceToDevice, s));
   if (p->failed || !p->comm) return comm_check(p);
   SHT_COMM_LOG("rank %d: all-to-all %s: group start\n", p->rank, from_x ? "X->Y" : "Y->X");
   SHT_NCCL_TRY(ncclGroupStart());
   for (int k = 1; k < P; ++k) {
     const int to = (r + k) % P, from = (r - k + P) % P;
-    if (srows[to] > 0)
-      SHT_NCCL_TRY(ncclSend(src + soff[to] * rowd, srows[to] * rowd, ncclDouble, to, p->comm, s));
-    if (drows[from] > 0)
-      SHT_NCCL_TRY(ncclRecv(dst + doff[from] * rowd, drows[from] * rowd, ncclDouble, from, p->comm, s));
+    for (int b = 0; b < nblk; ++b) {  // one message per field block
+      if (srows[to] > 0)
+        SHT_NCCL_TRY(ncclSend(src + b * sbs + soff[to] * rowd, srows[to] * rowd, ncclDouble, to, p->comm, s));
+      if (drows[from] > 0)
+        SHT_NCCL_TRY(ncclRecv(dst + b * dbs + doff[from] * rowd, drows[from] * rowd, ncclDouble, from, p->comm, s));
+    }
   }
   return nccl_settle(p, ncclGroupEnd(), "ncclGroupEnd (transposition)");
 }

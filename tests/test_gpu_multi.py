@@ -6,7 +6,7 @@
   grid <-> spectral transposition -- p2p (kernels store into the peers'
   buffers over NVLink, flag handshakes) and NCCL grouped send/recv in the
   reference's rotated order (collectives.py:85-86) -- and for the recompute
-  Legendre mode;
+  Legendre mode, and for both Fourier-row layouts (classic, field-blocked);
 * failure: one rank dies after plan creation; the survivors must raise
   ProtocolError from their bounded wait instead of hanging
   (tools/mp_fail_check.py; the reference's first-error abort,
@@ -40,14 +40,18 @@ def _torchrun(nproc, script, args, env_extra, port, timeout=900):
     return res
 
 
-@pytest.mark.parametrize("nproc,transport,recompute", [(2, "p2p", 0), (2, "nccl", 0), (2, "p2p", 1),
-                                                        (4, "p2p", 0), (4, "nccl", 0)])
-def test_torchrun_parity(nproc, transport, recompute):
+@pytest.mark.parametrize("nproc,transport,recompute,layout", [
+    (2, "p2p", 0, ""), (2, "nccl", 0, ""), (2, "p2p", 1, ""), (4, "p2p", 0, ""), (4, "nccl", 0, ""),
+    # field-blocked Fourier rows (chosen automatically past the remote-store cliff, sht_internal.h)
+    (2, "p2p", 0, "blocked"), (4, "p2p", 0, "blocked"), (4, "p2p", 1, "blocked")])
+def test_torchrun_parity(nproc, transport, recompute, layout):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    port = 29600 + 10 * nproc + (transport == "nccl") + 2 * recompute
-    res = _torchrun(nproc, "mp_check.py", ["79", "6", "319", "5", "639", "4"],
-                    {"SHT_TRANSPORT": transport, "SHT_RECOMPUTE": str(recompute), "MP_PAIRS": "4"}, port)
+    port = 29600 + 10 * nproc + (transport == "nccl") + 2 * recompute + 4 * (layout == "blocked")
+    env = {"SHT_TRANSPORT": transport, "SHT_RECOMPUTE": str(recompute), "MP_PAIRS": "4"}
+    if layout:
+        env["SHT_ROW_LAYOUT"] = layout
+    res = _torchrun(nproc, "mp_check.py", ["79", "6", "319", "70", "639", "4"], env, port)
     assert res.returncode == 0
     assert "MP_OK" in res.stdout
 
