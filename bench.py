@@ -399,6 +399,7 @@ def run_ours(args):
     t_leg_roof = F_leg / (pk["fp64_tflops"] * 1e12) * 1e3
     t_fft_roof = B_fft / (pk["hbm_gbs"] * 1e9) * 1e3
     transport = sh.transport
+    row_layout = sh.row_layout
     t_a2a_roof = B_a2a / (pk["nvlink_gbs"] * 1e9) * 1e3 if world > 1 else 0.0
     p2p = transport == "p2p"
     # p2p: the NVLink stores run inside the producing kernels (leg_inv -> ring owners, fft_g2f -> m
@@ -455,6 +456,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args),
             "layout": {"parallelism": f"m/ring-pair sharded x{world}, transposition: {transport}",
+                       "fourier_rows": row_layout,
                        "transport_env": os.environ.get("SHT_TRANSPORT", "p2p (default)"),
                        "gp_layout": args.gp_layout or "ring pairs (no grid-point transposition)",
                        "legendre": "recomputed per transform" if args.recompute_legendre else "stored table",

@@ -103,11 +103,13 @@ int sht_work(const sht_plan* plan, double* legendre_flops, double* fft_bytes, do
 /* Number of libsht kernel launches one inverse+direct pair issues. */
 int sht_kernel_launches(const sht_plan* plan, int* per_pair);
 
-/* Transport of the grid <-> spectral transposition: *p2p = 1 when the
- * kernels store the Fourier rows straight into the peers' receive buffers
+/* Transport of the grid <-> spectral transposition: bit 0 of *p2p = 1 when
+ * the kernels store the Fourier rows straight into the peers' receive buffers
  * over NVLink (CUDA IPC mappings, flag handshakes; the default whenever every
  * rank can map every peer), 0 for NCCL grouped send/recv between the kernels
- * (SHT_TRANSPORT=nccl, or one rank). */
+ * (SHT_TRANSPORT=nccl, or one rank); bit 1 = 1 when the Fourier-row buffers
+ * use the field-blocked layout (64-field blocks; p2p past the remote-store
+ * cliff, or SHT_ROW_LAYOUT=blocked). */
 int sht_transport(const sht_plan* plan, int* p2p);
 
 /* 128-byte NCCL unique id (call on rank 0 only). */

@@ -1501,7 +1501,7 @@ int sht_gp_bands(int truncation, int ndgl, const int32_t* nloen, int nA, int32_t
 
 int sht_transport(const sht_plan* p, int* p2p) {
   if (!p) return fail(SHT_ERR_CONFIG, "plan is NULL");
-  if (p2p) *p2p = p->p2p ? 1 : 0;
+  if (p2p) *p2p = (p->p2p ? 1 : 0) | (p->fblk ? 2 : 0);
   return SHT_OK;
 }
 

@@ -175,7 +175,15 @@ class SHTransform:
         'nccl' (grouped send/recv) or 'local' (one rank)."""
         n = C.c_int32()
         _lib.check(self._lib.sht_transport(self._plan, C.byref(n)))
-        return "p2p" if n.value else ("nccl" if self.nranks > 1 else "local")
+        return "p2p" if n.value & 1 else ("nccl" if self.nranks > 1 else "local")
+
+    @property
+    def row_layout(self) -> str:
+        """'classic' (a Fourier row holds every field) or 'field-blocked' (64-field
+        blocks; the p2p transposition past the remote-store cliff), sht_internal.h."""
+        n = C.c_int32()
+        _lib.check(self._lib.sht_transport(self._plan, C.byref(n)))
+        return "field-blocked" if n.value & 2 else "classic"
 
     def phase_ms(self, npairs: int = 1) -> dict:
         """Device times (ms) per phase, averaged over the last ``npairs`` (<= 64)
