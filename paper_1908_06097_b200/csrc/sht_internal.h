@@ -145,6 +145,7 @@ struct FftRing {       // one northern ring (and its southern mirror) on this ra
   int64_t goff_s;      // offset of the southern ring in the local grid field
   int64_t yrow_off;    // offset into yrow[] of this ring's (M_i + 1) Fourier rows
   int64_t tw_off;      // arena offset of this ring's twiddle table (ntw entries)
+  int64_t dit_off;     // offset of this ring's digit-reversed positions (N entries) in FftParams::ditpos, -1 if none
   int32_t ntw;
   int32_t shift;       // pruned whole-ring Bluestein: bins k > M of the spectrum sit at k + L - N (else 0)
   double w;            // Gaussian weight
@@ -164,6 +165,7 @@ struct FftParams {
   const FftStep* steps;
   const FftWork* work;
   const double2* tw;         // twiddle / chirp arena
+  const int32_t* ditpos;     // per non-Bluestein ring: position of spectrum bin k after the DIT steps
   double* const* rows_out;   // g2f: Fourier row (field block 0) of (ring, m) in the m-owner's receive buffer
   const int64_t* rows_out_bs;    // its field-block stride (doubles)
   const double* const* rows_in;  // f2g: Fourier row (field block 0) of (ring, m) in this rank's receive buffer

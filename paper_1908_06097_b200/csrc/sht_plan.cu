@@ -218,6 +218,7 @@ struct sht_plan {
   size_t fft_smem[sht::kFftVariants] = {};
   sht::FftStep* d_steps = nullptr;
   double2* d_tw = nullptr;
+  int32_t* d_ditpos = nullptr;
   ncclComm_t comm = nullptr;
   bool have_events = false;
   cudaEvent_t ev[10];                      // ev[8], ev[9]: set-up timing
@@ -291,7 +292,7 @@ static void free_plan(sht_plan* p) {
   }
   void* ptrs[] = {p->d_mu, p->d_sint, p->d_ptab, p->d_lm_m, p->d_lm_i0, p->d_lm_kp, p->d_xbase, p->d_lm_poff,
                   p->d_lm_soff, p->d_tiles_inv, p->d_tiles_dir, p->d_counter, p->X, p->d_steps, p->d_lm_poff_rc, p->d_dmant, p->d_dexp,
-                  p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->flagw, p->d_peer_flags,
+                  p->Y == p->X ? nullptr : p->Y, p->d_rings, p->d_work, p->d_tw, p->d_ditpos, p->flagw, p->d_peer_flags,
                   p->d_ring_out, p->d_rows_out, (void*)p->d_rows_in, p->d_gp_send_idx, p->d_gp_recv_idx,
                   p->d_gp_send_displ, p->d_gp_recv_displ, p->d_gridR, p->d_gp_buf0, p->d_gp_buf1, p->d_stage,
                   p->d_ring_bs, p->d_rows_out_bs};
@@ -800,6 +801,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   const int nlr = (int)p->my_rings.size();
   std::vector<FftRing> rings(nlr);
   std::vector<double2> arena;
+  std::vector<int32_t> ditpos;  // digit-reversed bin positions of the non-Bluestein rings
   p->yrow.clear();
   p->orow.clear();
   p->orow_owner.clear();
@@ -831,6 +833,11 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
     int variant = rp.variant;
     R.L = rp.L;
     R.shift = rp.shift;
+    R.dit_off = -1;
+    if (!rp.ring_blue) {
+      R.dit_off = (int64_t)ditpos.size();
+      for (int k = 0; k < R.n; ++k) ditpos.push_back((int32_t)fft_pos(k, rp.radices));
+    }
     R.mag_N = ((uint64_t)1 << 40) / (uint64_t)R.n + 1;
     R.mag_M1 = ((uint64_t)1 << 40) / (uint64_t)(R.mcap + 1) + 1;
     R.mag_L = ((uint64_t)1 << 40) / (uint64_t)R.L + 1;
@@ -936,6 +943,7 @@ static int build_plan(sht_plan* p, const void* nccl_id, bool dry_run = false) {
   if (int rc = upload(&p->d_work, work)) return rc;
   if (int rc = upload(&p->d_steps, steps)) return rc;
   if (int rc = upload(&p->d_tw, arena)) return rc;
+  if (int rc = upload(&p->d_ditpos, ditpos)) return rc;
   SHT_CUDA_TRY(cudaMalloc((void**)&p->d_counter, 4 * sizeof(int)));
   const size_t rowb = (size_t)p->nfb * kRowDbl * sizeof(double);  // one row in every field block
   SHT_CUDA_TRY(cudaMalloc((void**)&p->X, std::max<int64_t>(p->xtot, 1) * rowb));
@@ -1050,6 +1058,7 @@ static FftParams fft_params(const sht_plan* p) {
   fp.steps = p->d_steps;
   fp.work = p->d_work;
   fp.tw = p->d_tw;
+  fp.ditpos = p->d_ditpos;
   fp.rows_out = p->d_rows_out;
   fp.rows_in = p->d_rows_in;
   fp.rows_out_bs = p->d_rows_out_bs;
