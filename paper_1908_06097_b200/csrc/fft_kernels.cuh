@@ -664,28 +664,14 @@ __global__ void __launch_bounds__(FftCfg<V>::kThreads, FftCfg<V>::kMinBlocks)
           __stcs(g + rg.goff_s + k, -r.y);
         }
       }
-    } else {  // digit-reversed positions from the ring's table (L2), 4 in flight per thread
-      constexpr int U = 4;
-      const int tot = nseq * N;
-      const int32_t* dp = p.ditpos + rg.dit_off;
-      for (int i0 = threadIdx.x; i0 < tot; i0 += U * NT) {
-        int pos[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = i0 + u * NT;
-          const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
-          pos[u] = idx < tot ? q * L + __ldg(dp + k) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = i0 + u * NT;
-          if (idx >= tot || (p.debug & 4)) continue;
-          const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
-          const double2 r = buf[px(pos[u])];
-          double* g = grid + (int64_t)(fb + q) * p.grid_ld;
-          __stcs(g + rg.goff_n + k, r.x);
-          __stcs(g + rg.goff_s + k, -r.y);
-        }
+    } else {  // (the per-ring position table measured no faster than dit_pos here)
+      for (int idx = threadIdx.x; idx < nseq * N; idx += NT) {
+        const int q = fdiv(idx, rg.mag_N), k = idx - q * N;
+        const double2 r = buf[px(q * L + dit_pos(k, rs.st, rg.nstep))];
+        if (p.debug & 4) continue;
+        double* g = grid + (int64_t)(fb + q) * p.grid_ld;
+        __stcs(g + rg.goff_n + k, r.x);
+        __stcs(g + rg.goff_s + k, -r.y);
       }
     }
     __syncthreads();
