@@ -149,7 +149,7 @@ __device__ __forceinline__ InvTile inv_tile(const LegParams& p, const double* sp
   return c;
 }
 
-template <bool kStaged>
+template <bool kStaged, bool kBlk>  // pusher epilogue; field-blocked Fourier rows (sht_internal.h)
 __global__ void __launch_bounds__(kInvThreads, 1)
     leg_inv_kernel(const LegParams p, const double* __restrict__ spec, double* __restrict__ four) {
   extern __shared__ __align__(128) double sm[];
@@ -195,8 +195,8 @@ __global__ void __launch_bounds__(kInvThreads, 1)
         for (int a = 0; a < 4; ++a) {
           const int r = r0 + a;
           if (r >= c.nrows) break;
-          double* dst = p.ring_out[c.r0 + r] + (c.f0 >> p.fsh) * p.ring_bs[c.r0 + r] + c.lm * p.row_ld +
-                        (c.f0 & p.fmask) * 4;
+          double* dst = p.ring_out[c.r0 + r] + (kBlk ? (c.f0 >> 6) * p.ring_bs[c.r0 + r] + (int64_t)c.lm * kRowDbl
+                                                     : c.lm * p.row_ld + c.f0 * 4);
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
             const int f = lane + 32 * b;
@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(kInvThreads, 1)
     for (int g = 0; g < 4; ++g) {
       const int ring = c.r0 + roff + g * 8 + (lane >> 2);
       dst_row[g] = (active && !staged && g < gmax && ring < p.nh)
-                       ? p.ring_out[ring] + (c.f0 >> p.fsh) * p.ring_bs[ring] + c.lm * p.row_ld + (c.f0 & p.fmask) * 4
+                       ? p.ring_out[ring] + (kBlk ? (c.f0 >> 6) * p.ring_bs[ring] + (int64_t)c.lm * kRowDbl
+                                                  : c.lm * p.row_ld + c.f0 * 4)
                        : nullptr;
     }
 
@@ -652,14 +653,16 @@ void launch_leg_inv(const LegParams& p, const double* spec, double* four, int gr
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 64 || !(done >> dev & 1)) {
-    cudaFuncSetAttribute(leg_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
-    cudaFuncSetAttribute(leg_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
+    cudaFuncSetAttribute(leg_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leg_inv_smem());
     if (dev < 64) done |= 1ull << dev;
   }
-  if (p.stage)
-    leg_inv_kernel<true><<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
-  else
-    leg_inv_kernel<false><<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
+  const bool blk = p.fsh == 6;
+  auto k = p.stage ? (blk ? leg_inv_kernel<true, true> : leg_inv_kernel<true, false>)
+                   : (blk ? leg_inv_kernel<false, true> : leg_inv_kernel<false, false>);
+  k<<<grid, kInvThreads, leg_inv_smem(), s>>>(p, spec, four);
 }
 
 void launch_leg_dir(const LegParams& p, const double* four, double* spec, int grid, cudaStream_t s) {
@@ -676,8 +679,10 @@ void launch_leg_dir(const LegParams& p, const double* four, double* spec, int gr
 
 void leg_preload() {  // see fft_preload
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, leg_inv_kernel<false>);
-  cudaFuncGetAttributes(&a, leg_inv_kernel<true>);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<false, false>);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<true, false>);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<false, true>);
+  cudaFuncGetAttributes(&a, leg_inv_kernel<true, true>);
   cudaFuncGetAttributes(&a, leg_dir_kernel);
   cudaFuncGetAttributes(&a, leg_poly_kernel);
   cudaFuncGetAttributes(&a, leg_diag_kernel);
